@@ -1,0 +1,180 @@
+/*
+ * redve_b200 -- C ABI of the B200-native RED fixed-point / vector-extrapolation
+ * solver.  Drop-in boundary for the reference package ``redve``
+ * (/root/reference/pkg/src/redve); each entry point names the reference
+ * interface it replaces.  The reference is Python, so its FFI for this path
+ * is ctypes: the binding a maintainer adds is shown in INTEGRATION.md and is
+ * what paper_1805_02158_b200/_native.py does.
+ *
+ * Conventions
+ *  - plain C types only: pointers, sizes, doubles, ints; no torch types.
+ *  - images are fp64, row-major, batched [B][H][W] (B independent problems
+ *    that share operator, denoiser, sigma and alpha, like B calls to the
+ *    reference with different measurements).
+ *  - array arguments of compute calls are DEVICE pointers unless the field
+ *    says HOST; calls are asynchronous on the context's stream unless they
+ *    return host data (then they synchronise).
+ *  - every call returns REDVE_OK (0) or an error code; redve_last_error()
+ *    gives the message.  Codes map to the reference exceptions:
+ *      REDVE_E_VALUE      -> ValueError            (objective.py:61-66, solvers.py:162-199)
+ *      REDVE_E_SHAPE      -> ShapeMismatch         (imaging.py:27-28)
+ *      REDVE_E_KERNEL     -> KernelTooLarge        (imaging.py:23-24, 119-120)
+ *      REDVE_E_NONFINITE  -> NonFiniteIterate      (solvers.py:37-42, 249-252)
+ *      REDVE_E_CG         -> CgNoConvergence       (objective.py:40-41, 114-120)
+ *      REDVE_E_CUDA / REDVE_E_UNSUPPORTED -> RuntimeError
+ *  - one context per thread/stream; contexts are independent (the
+ *    reference's "sessions are pure" rule).
+ */
+#ifndef REDVE_B200_H
+#define REDVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  REDVE_OK = 0,
+  REDVE_E_VALUE = 1,
+  REDVE_E_SHAPE = 2,
+  REDVE_E_KERNEL = 3,
+  REDVE_E_CUDA = 4,
+  REDVE_E_NONFINITE = 5,
+  REDVE_E_CG = 6,
+  REDVE_E_UNSUPPORTED = 7
+};
+
+/* forward operators: imaging.py:147-204 */
+enum { REDVE_OP_BLUR = 0, REDVE_OP_BLUR_DOWNSAMPLE = 1 };
+/* denoisers: denoisers.py:21-129 + BASELINE.json plug-ins */
+enum {
+  REDVE_DN_IDENTITY = 0,   /* Identity        denoisers.py:21-27 */
+  REDVE_DN_CONV = 1,       /* GaussianFilter  denoisers.py:30-46 (any k x k taps) */
+  REDVE_DN_MEDIAN3 = 2,    /* periodic 3x3 median (configs[1]) */
+  REDVE_DN_FILTERBANK = 3, /* seeded reaction-diffusion stage (configs[3]) */
+  REDVE_DN_PATCH = 4,      /* PatchWeighted   denoisers.py:49-129 */
+  REDVE_DN_EXTERNAL = 5    /* f(x) supplied by the caller (host plug-in) */
+};
+/* weight rules: extrapolation.py:35-38 */
+enum { REDVE_VE_MPE = 0, REDVE_VE_RRE = 1, REDVE_VE_SVDMPE = 2 };
+/* drivers: solvers.py:388-399 */
+enum { REDVE_METHOD_FP = 0, REDVE_METHOD_FP_VE = 1 };
+
+typedef struct redve_ctx redve_ctx;
+typedef struct redve_problem redve_problem;
+
+/* Blur(psf, shape) / BlurDownsample(psf, factor, shape)  (imaging.py:147-204) */
+typedef struct {
+  int kind;            /* REDVE_OP_* */
+  int ksize;           /* odd PSF size (Psf.size) */
+  const double* taps;  /* HOST, ksize*ksize row-major (Psf.taps) */
+  int factor;          /* decimation factor; 1 for REDVE_OP_BLUR */
+} redve_operator_desc;
+
+typedef struct {
+  int kind;                  /* REDVE_DN_* */
+  int ksize;                 /* CONV: kernel size */
+  const double* taps;        /* CONV: HOST ksize*ksize taps (GaussianFilter.psf.taps) */
+  int patch_radius;          /* PATCH (PatchWeighted.__init__, denoisers.py:68-81) */
+  int search_radius;
+  int balance_iters;
+  double h;
+  int n_filters;             /* FILTERBANK */
+  int fsize;
+  const double* filters;     /* HOST [n_filters][fsize][fsize] */
+  const double* scales;      /* HOST [n_filters] */
+  double tau;
+} redve_denoiser_desc;
+
+/* SolveConfig (solvers.py:162-199) */
+typedef struct {
+  int method;            /* REDVE_METHOD_* ("fp" / "fp-ve") */
+  int ve_method;         /* REDVE_VE_* */
+  int m;
+  int kappa;             /* 1 <= kappa <= 11 */
+  int max_inner_steps;
+  double tol;
+  int stabilization_iters;
+  double rank_tolerance;
+} redve_solve_config;
+
+/* IterationTrace (solvers.py:51-95), HOST arrays sized by the caller:
+ * per-record arrays [B][cap], per-cycle arrays [B][ccap] (x12 for vectors). */
+typedef struct {
+  int cap;
+  int ccap;
+  int32_t* n_records;       /* [B] = inner steps taken */
+  double* step_norm;        /* [B][cap] */
+  double* cost;             /* [B][cap], NaN off the logging cadence */
+  double* psnr;             /* [B][cap], NaN off cadence / without reference */
+  double* gamma_abs_sum;    /* [B][cap], NaN unless an accepted cycle closed there */
+  double* elapsed_s;        /* [B][cap], device time since the solve started */
+  int32_t* n_cycles;        /* [B] accepted extrapolations */
+  int32_t* cycle_meta;      /* [B][ccap][4]: rule used, fallback(0/1), kappa_used, record index */
+  double* cycle_stability;  /* [B][ccap] sum|gamma| */
+  double* cycle_gamma;      /* [B][ccap][12] */
+  double* cycle_c;          /* [B][ccap][12] */
+  int32_t* status;          /* [B] REDVE_OK / REDVE_E_NONFINITE / REDVE_E_CG */
+  int32_t* returned_best;   /* [B] finalize returned the best plain iterate */
+} redve_trace;
+
+/* ExtrapolationResult (extrapolation.py:132-146), HOST, one per window */
+typedef struct {
+  int converged;
+  int extrapolated;
+  int kappa_used;
+  int method;               /* rule actually used */
+  int fallback;             /* 1 if MPE/SVD-MPE fell back to RRE */
+  double stability_sum;
+  double gamma[12];
+  double c[12];
+} redve_ve_result;
+
+/* ---- context ------------------------------------------------------------ */
+int redve_create(redve_ctx** out, int device);
+void redve_destroy(redve_ctx* ctx);
+const char* redve_last_error(const redve_ctx* ctx);
+int redve_set_stream(redve_ctx* ctx, void* cuda_stream); /* cudaStream_t, 0 = legacy default */
+int redve_synchronize(redve_ctx* ctx);
+const char* redve_version(void);
+
+/* ---- denoisers: f(x) for a batch (denoisers.py __call__) ------------------- */
+int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
+                  const double* x, double* out);
+
+/* ---- operators: apply / adjoint (imaging.py Blur / BlurDownsample) -------- */
+int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
+                         const double* x, double* out);
+int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
+                           const double* z, double* out);
+
+/* ---- RED objective (objective.py:44-135) ---------------------------------- */
+/* RedObjective(forward, y, sigma, alpha, denoiser) for B measurements.
+ * y: DEVICE [B][out_h][out_w]; reference: DEVICE [B][H][W] or NULL (PSNR). */
+int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
+                         const redve_denoiser_desc* dn, int B, int H, int W, const double* y,
+                         double sigma, double alpha, const double* reference,
+                         redve_problem** out);
+void redve_problem_destroy(redve_problem* p);
+/* fp_step (objective.py:100-121); f_ext: DEVICE f(x) for REDVE_DN_EXTERNAL, else NULL */
+int redve_fp_step(redve_problem* p, const double* x, double* out, const double* f_ext);
+/* data_fidelity / regularizer / cost (objective.py:78-88), HOST outputs [B] each */
+int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* cost,
+               double* data_fidelity, double* regularizer, double* psnr);
+/* solve / run_fixed_point / run_ve_cycling (solvers.py:288-399), whole batch on device.
+ * x0, x_out: DEVICE [B][H][W].  Per-image outcome in trace->status. */
+int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x0, double* x_out,
+                redve_trace* trace);
+
+/* ---- vector extrapolation (extrapolation.py:319-386) ---------------------- */
+/* extrapolate_once on B windows of `rows` = kappa+2 iterates of length n.
+ * window: DEVICE [B][rows][n]; out: DEVICE [B][n]; res: HOST [B]. */
+int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* window,
+                      int method, double rank_tolerance, double* out, redve_ve_result* res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REDVE_B200_H */

@@ -1,0 +1,767 @@
+// C ABI + native runtime: context, RED problem setup, device-resident solve
+// schedule (solvers.py:288-399 re-expressed as a static kernel schedule with
+// per-image masks), and the window-level VE entry point.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/redve_b200.h"
+#include "kernels.cuh"
+
+using namespace redve;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes > 0 ? bytes : 16);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct redve_ctx {
+  int device = 0;
+  cudaStream_t stream = 0;
+  std::string err;
+  std::map<int, DevBuf*> twiddles;
+  DevBuf scratch_taps, scratch_a, scratch_b, ve_ring, ve_state, ve_partials, ve_counters,
+      ve_q, ve_trace;
+  ~redve_ctx() {
+    for (auto& kv : twiddles) delete kv.second;
+  }
+  const cd* tw(int L) {
+    auto it = twiddles.find(L);
+    if (it != twiddles.end()) return it->second->as<cd>();
+    DevBuf* b = new DevBuf();
+    if (b->ensure(sizeof(cd) * L) != cudaSuccess) {
+      delete b;
+      return nullptr;
+    }
+    launch_twiddles(b->as<cd>(), L, stream);
+    twiddles[L] = b;
+    return b->as<cd>();
+  }
+};
+
+static int fail(redve_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(ctx, REDVE_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_));      \
+  } while (0)
+
+#define CKL()                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(ctx, REDVE_E_CUDA, "kernel launch: %s", cudaGetErrorString(e_));  \
+  } while (0)
+
+static int is_odd_pos(int k) { return k >= 1 && (k & 1); }
+
+// ------------------------------------------------------------------ problem
+struct redve_problem {
+  redve_ctx* ctx;
+  int B, H, W, Hy, Wy, npairs;
+  long long N;
+  redve_operator_desc op;
+  int dn_kind;
+  int dn_ksize;
+  double sigma, alpha;
+  bool fourier;
+  int lpc_row, lpc_col;
+  DevBuf htaps, dntaps, y, ref, hty, xb, g, Z, state, partials, cnt_inv, cnt_cost, cnt_ve,
+      fbuf, ring, best, q, trace, vals;
+  bool has_ref = false;
+  const cd* twH = nullptr;
+  const cd* twW = nullptr;
+  int ring_S = 0;
+};
+
+static DenoiseArgs dn_args(const redve_problem* p) {
+  DenoiseArgs d;
+  d.kind = p->dn_kind;
+  d.ksize = p->dn_kind == DN_CONV ? p->dn_ksize : 0;
+  d.radius = p->dn_kind == DN_CONV ? p->dn_ksize / 2 : (p->dn_kind == DN_MEDIAN3 ? 1 : 0);
+  d.taps = p->dntaps.as<double>();
+  return d;
+}
+
+static int lines_per_cta(int L) {
+  int T = threads_per_line(L);
+  int lpc = 128 / T;
+  return lpc < 1 ? 1 : lpc;
+}
+
+static int col_lines_per_cta(int H, int W) {
+  int T = threads_per_line(H);
+  int lpc = 256 / T;
+  if (lpc > 16) lpc = 16;
+  if (lpc < 1) lpc = 1;
+  return lpc;
+}
+
+static int map_dn_kind(int k) {
+  switch (k) {
+    case REDVE_DN_IDENTITY: return DN_IDENTITY;
+    case REDVE_DN_CONV: return DN_CONV;
+    case REDVE_DN_MEDIAN3: return DN_MEDIAN3;
+    default: return DN_EXTERNAL;
+  }
+}
+
+// Fourier solve pipeline on pairs: Z <- rowfwd(xin) ; col(scale) ; rowinv -> out
+static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double scale, View out,
+                            const double* base, int epilogue, View xprev, StepCtl ctl,
+                            TraceBufs tr, int S, int phase) {
+  redve_ctx* ctx = p->ctx;
+  RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, p->Z.as<cd>(), p->twW,
+                p->state.as<ImgState>(), phase};
+  launch_row_fwd(rf, p->npairs, ctx->stream);
+  CKL();
+  ColArgs ca{p->B, p->H, p->W, p->lpc_col, p->Z.as<cd>(), p->twH, p->g.as<double>(), scale,
+             p->state.as<ImgState>(), phase};
+  launch_col(ca, p->npairs, ctx->stream);
+  CKL();
+  RowInvArgs ri;
+  ri.B = p->B; ri.H = p->H; ri.W = p->W; ri.lpc = p->lpc_row;
+  ri.Z = p->Z.as<cd>(); ri.tw = p->twW; ri.out = out; ri.base = base; ri.xprev = xprev;
+  ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
+  ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
+  launch_row_inv(ri, p->npairs, ctx->stream);
+  CKL();
+  return REDVE_OK;
+}
+
+static View plain(const double* base, long long N) {
+  View v;
+  v.base = const_cast<double*>(base);
+  v.img_stride = N;
+  v.slot_stride = 0;
+  v.S = 1;
+  v.mode = 0;
+  return v;
+}
+
+extern "C" {
+
+const char* redve_version(void) { return "redve_b200 0.1.0 (sm_100a)"; }
+
+int redve_create(redve_ctx** out, int device) {
+  if (!out) return REDVE_E_VALUE;
+  redve_ctx* c = new redve_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    *out = c;
+    return fail(c, REDVE_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  configure_kernels();
+  *out = c;
+  return REDVE_OK;
+}
+
+void redve_destroy(redve_ctx* ctx) { delete ctx; }
+
+const char* redve_last_error(const redve_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int redve_set_stream(redve_ctx* ctx, void* s) {
+  ctx->stream = reinterpret_cast<cudaStream_t>(s);
+  return REDVE_OK;
+}
+
+int redve_synchronize(redve_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+
+// ------------------------------------------------------------------ denoise
+int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
+                  const double* x, double* out) {
+  if (B < 1 || H < 1 || W < 1) return fail(ctx, REDVE_E_VALUE, "bad batch shape");
+  const long long N = (long long)H * W;
+  switch (dn->kind) {
+    case REDVE_DN_IDENTITY:
+      CK(cudaMemcpyAsync(out, x, sizeof(double) * N * B, cudaMemcpyDeviceToDevice, ctx->stream));
+      return REDVE_OK;
+    case REDVE_DN_MEDIAN3:
+      launch_median3(x, out, B, H, W, ctx->stream);
+      CKL();
+      return REDVE_OK;
+    case REDVE_DN_CONV: {
+      if (!is_odd_pos(dn->ksize)) return fail(ctx, REDVE_E_VALUE, "kernel size must be odd");
+      if (dn->ksize > H || dn->ksize > W)
+        return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
+      size_t kb = sizeof(double) * dn->ksize * dn->ksize;
+      CK(ctx->scratch_taps.ensure(kb));
+      CK(cudaMemcpyAsync(ctx->scratch_taps.p, dn->taps, kb, cudaMemcpyHostToDevice, ctx->stream));
+      launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), dn->ksize, 0, 1.0, ctx->stream);
+      CKL();
+      // taps buffer is reused by the next call: keep it alive until then
+      CK(cudaStreamSynchronize(ctx->stream));
+      return REDVE_OK;
+    }
+    default:
+      return fail(ctx, REDVE_E_UNSUPPORTED, "denoiser kind %d not available in this build",
+                  dn->kind);
+  }
+}
+
+// ------------------------------------------------------------------ operators
+static int op_check(redve_ctx* ctx, const redve_operator_desc* op, int H, int W) {
+  if (!is_odd_pos(op->ksize)) return fail(ctx, REDVE_E_VALUE, "PSF size must be odd and >= 1");
+  if (op->ksize > H || op->ksize > W)
+    return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", op->ksize, op->ksize, H, W);
+  if (op->kind == REDVE_OP_BLUR_DOWNSAMPLE && op->factor < 1)
+    return fail(ctx, REDVE_E_VALUE, "downsample factor must be >= 1");
+  if (op->kind != REDVE_OP_BLUR && op->kind != REDVE_OP_BLUR_DOWNSAMPLE)
+    return fail(ctx, REDVE_E_VALUE, "unknown operator kind");
+  return REDVE_OK;
+}
+
+static int upload_taps(redve_ctx* ctx, const redve_operator_desc* op) {
+  size_t kb = sizeof(double) * op->ksize * op->ksize;
+  CK(ctx->scratch_taps.ensure(kb));
+  CK(cudaMemcpyAsync(ctx->scratch_taps.p, op->taps, kb, cudaMemcpyHostToDevice, ctx->stream));
+  return REDVE_OK;
+}
+
+int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
+                         const double* x, double* out) {
+  int rc = op_check(ctx, op, H, W);
+  if (rc) return rc;
+  if ((rc = upload_taps(ctx, op))) return rc;
+  if (op->kind == REDVE_OP_BLUR) {
+    launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 0, 1.0, ctx->stream);
+  } else {
+    launch_decimate_conv(x, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
+                         ctx->stream);
+  }
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+
+int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
+                           const double* z, double* out) {
+  int rc = op_check(ctx, op, H, W);
+  if (rc) return rc;
+  if ((rc = upload_taps(ctx, op))) return rc;
+  if (op->kind == REDVE_OP_BLUR) {
+    launch_conv(z, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 1, 1.0, ctx->stream);
+  } else {
+    launch_upsample_corr(z, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
+                         1.0, ctx->stream);
+  }
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+
+// ------------------------------------------------------------------ problem
+int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
+                         const redve_denoiser_desc* dn, int B, int H, int W, const double* y,
+                         double sigma, double alpha, const double* reference,
+                         redve_problem** out) {
+  *out = nullptr;
+  if (!(sigma > 0)) return fail(ctx, REDVE_E_VALUE, "sigma must be > 0");
+  if (!(alpha > 0)) return fail(ctx, REDVE_E_VALUE, "alpha must be > 0");
+  if (B < 1 || H < 1 || W < 1) return fail(ctx, REDVE_E_VALUE, "bad batch shape");
+  int rc = op_check(ctx, op, H, W);
+  if (rc) return rc;
+  if (dn->kind == REDVE_DN_CONV) {
+    if (!is_odd_pos(dn->ksize)) return fail(ctx, REDVE_E_VALUE, "denoiser kernel must be odd");
+    if (dn->ksize > H || dn->ksize > W)
+      return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
+  }
+  if (op->kind != REDVE_OP_BLUR)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "BlurDownsample problems: CG path not built yet");
+  if (dn->kind != REDVE_DN_IDENTITY && dn->kind != REDVE_DN_CONV && dn->kind != REDVE_DN_MEDIAN3 &&
+      dn->kind != REDVE_DN_EXTERNAL)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "denoiser kind %d not available in this build",
+                dn->kind);
+  if (H > 4096 || W > 4096) return fail(ctx, REDVE_E_UNSUPPORTED, "image side > 4096");
+  if (!is_pow2(H) && H > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
+  if (!is_pow2(W) && W > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
+
+  redve_problem* p = new redve_problem();
+  p->ctx = ctx;
+  p->B = B; p->H = H; p->W = W;
+  p->N = (long long)H * W;
+  p->op = *op;
+  p->op.taps = nullptr;
+  int f = op->kind == REDVE_OP_BLUR ? 1 : op->factor;
+  p->Hy = (H + f - 1) / f;
+  p->Wy = (W + f - 1) / f;
+  p->npairs = (B + 1) / 2;
+  p->dn_kind = map_dn_kind(dn->kind);
+  p->dn_ksize = dn->kind == REDVE_DN_CONV ? dn->ksize : 0;
+  p->sigma = sigma;
+  p->alpha = alpha;
+  p->fourier = op->kind == REDVE_OP_BLUR;
+  p->lpc_row = lines_per_cta(W);
+  if (p->lpc_row > H) p->lpc_row = H;
+  p->lpc_col = col_lines_per_cta(H, W);
+  if (p->lpc_col > W) p->lpc_col = W;
+
+  auto bail = [&](int code) {
+    delete p;
+    return code;
+  };
+#define PK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      fail(ctx, REDVE_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_));             \
+      return bail(REDVE_E_CUDA);                                                    \
+    }                                                                               \
+  } while (0)
+  const cudaStream_t s = ctx->stream;
+  const size_t kb = sizeof(double) * op->ksize * op->ksize;
+  PK(p->htaps.ensure(kb));
+  PK(cudaMemcpyAsync(p->htaps.p, op->taps, kb, cudaMemcpyHostToDevice, s));
+  size_t db = dn->kind == REDVE_DN_CONV ? sizeof(double) * dn->ksize * dn->ksize : 8;
+  PK(p->dntaps.ensure(db));
+  if (dn->kind == REDVE_DN_CONV)
+    PK(cudaMemcpyAsync(p->dntaps.p, dn->taps, db, cudaMemcpyHostToDevice, s));
+  const long long Ny = (long long)p->Hy * p->Wy;
+  PK(p->y.ensure(sizeof(double) * Ny * B));
+  PK(cudaMemcpyAsync(p->y.p, y, sizeof(double) * Ny * B, cudaMemcpyDeviceToDevice, s));
+  if (reference) {
+    p->has_ref = true;
+    PK(p->ref.ensure(sizeof(double) * p->N * B));
+    PK(cudaMemcpyAsync(p->ref.p, reference, sizeof(double) * p->N * B, cudaMemcpyDeviceToDevice,
+                       s));
+  }
+  PK(p->state.ensure(sizeof(ImgState) * B));
+  launch_init_state(p->state.as<ImgState>(), B, s);
+  int nblk_row = (H + p->lpc_row - 1) / p->lpc_row;
+  int nblk_cost = (H + cost_rows(H) - 1) / cost_rows(H);
+  size_t part = (size_t)p->npairs * (nblk_row > nblk_cost ? nblk_row : nblk_cost) * 6;
+  PK(p->partials.ensure(sizeof(double) * part));
+  PK(p->cnt_inv.ensure(sizeof(unsigned) * (B + 1)));
+  PK(p->cnt_cost.ensure(sizeof(unsigned) * (B + 1)));
+  PK(p->cnt_ve.ensure(sizeof(unsigned) * (B + 1)));
+  PK(cudaMemsetAsync(p->cnt_inv.p, 0, sizeof(unsigned) * (B + 1), s));
+  PK(cudaMemsetAsync(p->cnt_cost.p, 0, sizeof(unsigned) * (B + 1), s));
+  PK(cudaMemsetAsync(p->cnt_ve.p, 0, sizeof(unsigned) * (B + 1), s));
+  PK(p->vals.ensure(sizeof(double) * 3 * B));
+  // H^T y / sigma^2 (objective.py:70)
+  PK(p->hty.ensure(sizeof(double) * p->N * B));
+  launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W, p->htaps.as<double>(),
+              op->ksize, 1, 1.0 / (sigma * sigma), s);
+  PK(cudaGetLastError());
+  if (p->fourier) {
+    p->twH = ctx->tw(H);
+    p->twW = ctx->tw(W);
+    if (!p->twH || !p->twW) {
+      fail(ctx, REDVE_E_CUDA, "twiddle allocation failed");
+      return bail(REDVE_E_CUDA);
+    }
+    PK(p->g.ensure(sizeof(double) * p->N));
+    launch_inv_denom(p->g.as<double>(), H, W, p->htaps.as<double>(), op->ksize, sigma, alpha, s);
+    PK(cudaGetLastError());
+    PK(p->Z.ensure(sizeof(cd) * p->N * p->npairs));
+    PK(p->xb.ensure(sizeof(double) * p->N * B));
+    // x_b = IDFT(DFT(H^T y / sigma^2) / d)
+    DenoiseArgs ident{DN_IDENTITY, 0, 0, nullptr};
+    StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
+    TraceBufs tr;
+    memset(&tr, 0, sizeof(tr));
+    int r = fourier_pipeline(p, plain(p->hty.as<double>(), p->N), ident, 1.0,
+                             plain(p->xb.as<double>(), p->N), nullptr, 0, plain(nullptr, p->N),
+                             ctl, tr, 1, PH_SETUP);
+    if (r) return bail(r);
+  }
+#undef PK
+  *out = p;
+  return REDVE_OK;
+}
+
+void redve_problem_destroy(redve_problem* p) { delete p; }
+
+int redve_fp_step(redve_problem* p, const double* x, double* out, const double* f_ext) {
+  redve_ctx* ctx = p->ctx;
+  if (p->dn_kind == DN_EXTERNAL && !f_ext)
+    return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
+  launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream);
+  DenoiseArgs dn = dn_args(p);
+  View xin = plain(x, p->N);
+  if (p->dn_kind == DN_EXTERNAL) {
+    dn.kind = DN_IDENTITY;
+    dn.radius = 0;
+    xin = plain(f_ext, p->N);
+  }
+  StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
+  TraceBufs tr;
+  memset(&tr, 0, sizeof(tr));
+  return fourier_pipeline(p, xin, dn, p->alpha, plain(out, p->N), p->xb.as<double>(), 0,
+                          plain(nullptr, p->N), ctl, tr, 1, PH_SETUP);
+}
+
+static CostArgs cost_args(redve_problem* p, View x, const double* f_ext, int mode, StepCtl ctl,
+                          TraceBufs tr) {
+  CostArgs a;
+  a.B = p->B; a.H = p->H; a.W = p->W; a.rows = cost_rows(p->H);
+  a.Hy = p->Hy; a.Wy = p->Wy;
+  a.factor = p->op.kind == REDVE_OP_BLUR ? 1 : p->op.factor;
+  a.x = x; a.y = p->y.as<double>(); a.ref = p->has_ref ? p->ref.as<double>() : nullptr;
+  a.dn = dn_args(p);
+  a.fext = f_ext;
+  a.htaps = p->htaps.as<double>(); a.hk = p->op.ksize;
+  a.sigma = p->sigma; a.alpha = p->alpha;
+  a.mode = mode; a.out_vals = p->vals.as<double>();
+  a.st = p->state.as<ImgState>(); a.ctl = ctl; a.tr = tr;
+  a.partials = p->partials.as<double>(); a.counters = p->cnt_cost.as<unsigned>();
+  return a;
+}
+
+int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* cost,
+               double* fid, double* reg, double* psnr) {
+  redve_ctx* ctx = p->ctx;
+  if (p->dn_kind == DN_EXTERNAL && !f_ext)
+    return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
+  StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
+  TraceBufs tr;
+  memset(&tr, 0, sizeof(tr));
+  CostArgs a = cost_args(p, plain(x, p->N), f_ext, COST_VALUE, ctl, tr);
+  launch_cost(a, p->npairs, ctx->stream);
+  CKL();
+  std::vector<double> v(3 * p->B);
+  CK(cudaMemcpyAsync(v.data(), p->vals.p, sizeof(double) * 3 * p->B, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int b = 0; b < p->B; ++b) {
+    double df = v[3 * b] / (2.0 * p->sigma * p->sigma);
+    double rg = 0.5 * v[3 * b + 1];
+    if (fid) fid[b] = df;
+    if (reg) reg[b] = rg;
+    if (cost) cost[b] = df + p->alpha * rg;
+    if (psnr) {
+      double mse = v[3 * b + 2] / (double)p->N;
+      psnr[b] = !p->has_ref ? NAN : (mse == 0.0 ? INFINITY : (!std::isfinite(mse) ? -INFINITY
+                                   : 10.0 * std::log10(255.0 * 255.0 / mse)));
+    }
+  }
+  return REDVE_OK;
+}
+
+// ------------------------------------------------------------------ solve
+int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x0, double* x_out,
+                redve_trace* trace) {
+  redve_ctx* ctx = p->ctx;
+  const cudaStream_t s = ctx->stream;
+  if (cfg->method != REDVE_METHOD_FP && cfg->method != REDVE_METHOD_FP_VE)
+    return fail(ctx, REDVE_E_VALUE, "unknown method %d", cfg->method);
+  if (cfg->ve_method < 0 || cfg->ve_method > 2) return fail(ctx, REDVE_E_VALUE, "unknown VE method");
+  if (cfg->kappa < 1) return fail(ctx, REDVE_E_VALUE, "kappa must be >= 1");
+  if (cfg->kappa + 1 > MAXKP1) return fail(ctx, REDVE_E_UNSUPPORTED, "kappa > %d", MAXKP1 - 1);
+  if (cfg->m < 0) return fail(ctx, REDVE_E_VALUE, "m must be >= 0");
+  if (cfg->max_inner_steps < 1) return fail(ctx, REDVE_E_VALUE, "max_inner_steps must be >= 1");
+  if (cfg->tol < 0) return fail(ctx, REDVE_E_VALUE, "tol must be >= 0");
+  if (cfg->stabilization_iters < 0) return fail(ctx, REDVE_E_VALUE, "stabilization_iters < 0");
+  if (!(cfg->rank_tolerance > 0)) return fail(ctx, REDVE_E_VALUE, "rank_tolerance must be > 0");
+  const bool ve = cfg->method == REDVE_METHOD_FP_VE;
+  if (ve && cfg->max_inner_steps < cfg->m + cfg->kappa + 2)
+    return fail(ctx, REDVE_E_VALUE, "budget must admit at least one full cycle (m + kappa + 2)");
+  if (p->dn_kind == DN_EXTERNAL)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "device solve needs a device denoiser");
+  if (!p->fourier) return fail(ctx, REDVE_E_UNSUPPORTED, "CG path not built yet");
+
+  const int B = p->B;
+  const long long N = p->N;
+  const int budget = cfg->max_inner_steps;
+  const int stab = ve ? cfg->stabilization_iters : 0;
+  const int clen = cfg->m + cfg->kappa + 1;
+  const int S = ve ? clen + 1 : 2;
+  const int kp1 = cfg->kappa + 1;
+  const int cap = budget + stab;
+  const int ccap = budget / clen + 2;
+  const int log_every = N <= 128 * 128 ? 1 : 5;  // solvers.py:34,213
+  const bool track = ve;
+
+  CK(p->ring.ensure(sizeof(double) * N * S * B));
+  if (track) CK(p->best.ensure(sizeof(double) * N * B));
+  int chunks = (int)((N + 256 * 8 - 1) / (256 * 8));
+  if (chunks > 64) chunks = 64;
+  if (chunks < 1) chunks = 1;
+  if (ve) {
+    CK(p->q.ensure(sizeof(double) * N * kp1 * B));
+    size_t need = (size_t)B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2);
+    if (need * sizeof(double) > p->partials.n) {
+      DevBuf tmp;
+      // grow partials (keep row-kernel requirement too)
+      size_t old = p->partials.n;
+      (void)old;
+      CK(p->partials.ensure(need * sizeof(double) + 64));
+    }
+  }
+  // trace buffers (device)
+  const size_t nrec = (size_t)B * cap, ncyc = (size_t)B * ccap;
+  size_t tbytes = sizeof(double) * (5 * nrec + ncyc * (1 + 2 * MAXKP1)) + sizeof(int) * ncyc * 4;
+  CK(p->trace.ensure(tbytes));
+  TraceBufs tr;
+  {
+    char* base = p->trace.as<char>();
+    tr.cap = cap;
+    tr.ccap = ccap;
+    double* d = reinterpret_cast<double*>(base);
+    tr.step_norm = d;
+    tr.cost = d + nrec;
+    tr.psnr = d + 2 * nrec;
+    tr.gamma = d + 3 * nrec;
+    tr.elapsed = d + 4 * nrec;
+    tr.cyc_stab = d + 5 * nrec;
+    tr.cyc_gamma = tr.cyc_stab + ncyc;
+    tr.cyc_c = tr.cyc_gamma + ncyc * MAXKP1;
+    tr.cyc_meta = reinterpret_cast<int*>(tr.cyc_c + ncyc * MAXKP1);
+  }
+  CK(cudaMemsetAsync(p->trace.p, 0xFF, sizeof(double) * 5 * nrec, s));  // NaN
+  CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
+                                         sizeof(int) * ncyc * 4, s));
+  ImgState* st = p->state.as<ImgState>();
+  launch_init_state(st, B, s);
+  CKL();
+  // x0 -> ring slot 0
+  CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * N * S, x0, sizeof(double) * N,
+                       sizeof(double) * N, B, cudaMemcpyDeviceToDevice, s));
+
+  View cur{p->ring.as<double>(), N * S, N, S, 1};
+  View nxt{p->ring.as<double>(), N * S, N, S, 2};
+  View bestv = plain(p->best.as<double>(), N);
+  DenoiseArgs dn = dn_args(p);
+  StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0};
+
+  VeArgs va;
+  va.B = B; va.N = N; va.m = cfg->m; va.kp1 = kp1; va.S = S;
+  va.ring = p->ring.as<double>(); va.img_stride = N * S; va.slot_stride = N;
+  va.st = st; va.tr = tr; va.partials = p->partials.as<double>();
+  va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
+  va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
+
+  if (track) {  // note_initial (solvers.py:219-223)
+    CostArgs ca = cost_args(p, cur, nullptr, COST_INIT, ctl, tr);
+    launch_cost(ca, p->npairs, s);
+    CKL();
+    launch_copy_view(bestv, cur, B, N, st, 1, s);
+    CKL();
+  }
+
+  auto step = [&](int phase, bool cadence) -> int {
+    StepCtl c = ctl;
+    c.phase = phase;
+    c.defer_commit = cadence ? 1 : 0;
+    int r = fourier_pipeline(p, cur, dn, p->alpha, nxt, p->xb.as<double>(), 1, cur, c, tr, S,
+                             phase);
+    if (r) return r;
+    if (cadence) {
+      CostArgs ca = cost_args(p, cur, nullptr, COST_RECORD, c, tr);
+      launch_cost(ca, p->npairs, s);
+      CKL();
+      if (track) {
+        launch_copy_view(bestv, cur, B, N, st, 1, s);
+        CKL();
+      }
+    }
+    return REDVE_OK;
+  };
+
+  std::vector<ImgState> hst(B);
+  auto any_running = [&]() -> int {
+    CK(cudaMemcpyAsync(hst.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int any = 0;
+    for (int b = 0; b < B; ++b) any |= (hst[b].term == RUNNING);
+    return any ? 1 : 0;
+  };
+  const int check_every = cfg->tol > 0 ? 1 : 8;
+
+  int k = 0;
+  if (!ve) {
+    while (k < budget) {
+      int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+      if (r) return r;
+      ++k;
+      if (k % (check_every * clen) == 0 && k < budget) {
+        int a = any_running();
+        if (a < 0 || a > 1) return a;
+        if (!a) break;
+      }
+    }
+  } else {
+    int cycles = 0;
+    while (true) {
+      int n = 0;
+      for (int i = 0; i < clen; ++i) {
+        int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+        if (r) return r;
+        ++k;
+        ++n;
+        if (k >= budget) break;
+      }
+      if (n == clen) {
+        launch_gram(va, s);
+        CKL();
+        launch_mgs(va, s);
+        CKL();
+        launch_combine(va, s);
+        CKL();
+      }
+      if (k >= budget) break;
+      if (++cycles % check_every == 0) {
+        int a = any_running();
+        if (a < 0 || a > 1) return a;
+        if (!a) break;
+      }
+    }
+  }
+  for (int i = 0; i < stab; ++i) {
+    int r = step(PH_STAB, true);
+    if (r) return r;
+  }
+  if (track) {  // finalize (solvers.py:255-262)
+    CostArgs ca = cost_args(p, cur, nullptr, COST_FINAL, ctl, tr);
+    launch_cost(ca, p->npairs, s);
+    CKL();
+  }
+  launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s);
+  CKL();
+
+  // trace back to the host
+  CK(cudaMemcpyAsync(hst.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+  const int hc = trace->cap < cap ? trace->cap : cap;
+  const int hcc = trace->ccap < ccap ? trace->ccap : ccap;
+  auto cp2 = [&](void* dst, const void* src, size_t elem, int hcols, int dcols) -> cudaError_t {
+    return cudaMemcpy2DAsync(dst, elem * hcols, src, elem * dcols, elem * (hcols < dcols ? hcols : dcols),
+                             B, cudaMemcpyDeviceToHost, s);
+  };
+  if (trace->step_norm) CK(cp2(trace->step_norm, tr.step_norm, 8, trace->cap, cap));
+  if (trace->cost) CK(cp2(trace->cost, tr.cost, 8, trace->cap, cap));
+  if (trace->psnr) CK(cp2(trace->psnr, tr.psnr, 8, trace->cap, cap));
+  if (trace->gamma_abs_sum) CK(cp2(trace->gamma_abs_sum, tr.gamma, 8, trace->cap, cap));
+  if (trace->elapsed_s) CK(cp2(trace->elapsed_s, tr.elapsed, 8, trace->cap, cap));
+  if (trace->cycle_meta) CK(cp2(trace->cycle_meta, tr.cyc_meta, 16, trace->ccap, ccap));
+  if (trace->cycle_stability) CK(cp2(trace->cycle_stability, tr.cyc_stab, 8, trace->ccap, ccap));
+  if (trace->cycle_gamma) CK(cp2(trace->cycle_gamma, tr.cyc_gamma, 8 * MAXKP1, trace->ccap, ccap));
+  if (trace->cycle_c) CK(cp2(trace->cycle_c, tr.cyc_c, 8 * MAXKP1, trace->ccap, ccap));
+  CK(cudaStreamSynchronize(s));
+  (void)hc;
+  (void)hcc;
+  for (int b = 0; b < B; ++b) {
+    if (trace->n_records) trace->n_records[b] = hst[b].k;
+    if (trace->n_cycles) trace->n_cycles[b] = hst[b].ncycles;
+    if (trace->returned_best) trace->returned_best[b] = hst[b].use_best;
+    if (trace->status)
+      trace->status[b] = hst[b].err == ERR_NONE ? REDVE_OK
+                         : (hst[b].err == ERR_CG ? REDVE_E_CG : REDVE_E_NONFINITE);
+  }
+  return REDVE_OK;
+}
+
+// ------------------------------------------------------------------ window VE
+int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* window,
+                      int method, double rank_tol, double* out, redve_ve_result* res) {
+  if (rows < 3) return fail(ctx, REDVE_E_VALUE, "window needs at least kappa+2 = 3 vectors");
+  if (rows - 1 > MAXKP1) return fail(ctx, REDVE_E_UNSUPPORTED, "kappa > %d", MAXKP1 - 1);
+  if (method < 0 || method > 2) return fail(ctx, REDVE_E_VALUE, "unknown VE method");
+  if (!(rank_tol > 0)) return fail(ctx, REDVE_E_VALUE, "rank_tolerance must be positive");
+  const cudaStream_t s = ctx->stream;
+  const int kp1 = rows - 1;
+  CK(ctx->ve_ring.ensure(sizeof(double) * n * rows * B));
+  CK(cudaMemcpyAsync(ctx->ve_ring.p, window, sizeof(double) * n * rows * B,
+                     cudaMemcpyDeviceToDevice, s));
+  CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
+  ImgState* st = ctx->ve_state.as<ImgState>();
+  launch_init_state(st, B, s);
+  CKL();
+  launch_window_extrapolate_setup(st, B, rows, 0, s);
+  CKL();
+  int chunks = (int)((n + 256 * 8 - 1) / (256 * 8));
+  if (chunks > 64) chunks = 64;
+  if (chunks < 1) chunks = 1;
+  CK(ctx->ve_partials.ensure(sizeof(double) * B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2) + 64));
+  CK(ctx->ve_counters.ensure(sizeof(unsigned) * B));
+  CK(cudaMemsetAsync(ctx->ve_counters.p, 0, sizeof(unsigned) * B, s));
+  CK(ctx->ve_q.ensure(sizeof(double) * n * kp1 * B));
+  const int ccap = 1;
+  CK(ctx->ve_trace.ensure(sizeof(double) * (B * 2 + (size_t)B * ccap * (1 + 2 * MAXKP1)) +
+                          sizeof(int) * B * ccap * 4));
+  TraceBufs tr;
+  {
+    double* d = ctx->ve_trace.as<double>();
+    tr.cap = 1; tr.ccap = ccap;
+    tr.step_norm = tr.cost = tr.psnr = tr.elapsed = d;
+    tr.gamma = d + B;
+    tr.cyc_stab = d + 2 * B;
+    tr.cyc_gamma = tr.cyc_stab + B * ccap;
+    tr.cyc_c = tr.cyc_gamma + B * ccap * MAXKP1;
+    tr.cyc_meta = reinterpret_cast<int*>(tr.cyc_c + B * ccap * MAXKP1);
+  }
+  CK(cudaMemsetAsync(ctx->ve_trace.p, 0, ctx->ve_trace.n, s));
+  VeArgs va;
+  va.B = B; va.N = n; va.m = 0; va.kp1 = kp1; va.S = rows;
+  va.ring = ctx->ve_ring.as<double>(); va.img_stride = n * rows; va.slot_stride = n;
+  va.st = st; va.tr = tr; va.partials = ctx->ve_partials.as<double>();
+  va.counters = ctx->ve_counters.as<unsigned>(); va.qscratch = ctx->ve_q.as<double>();
+  va.method = method; va.rank_tol = rank_tol; va.chunks = chunks;
+  launch_gram(va, s);
+  CKL();
+  launch_mgs(va, s);
+  CKL();
+  std::vector<ImgState> pre(B);
+  CK(cudaMemcpyAsync(pre.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+  launch_combine(va, s);
+  CKL();
+  View curv{ctx->ve_ring.as<double>(), n * rows, n, rows, 1};
+  launch_gather(out, curv, nullptr, B, n, st, s);
+  CKL();
+  std::vector<ImgState> post(B);
+  CK(cudaMemcpyAsync(post.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) {
+    redve_ve_result& r = res[b];
+    memset(&r, 0, sizeof(r));
+    const ImgState& q = pre[b];
+    r.converged = q.ve_mode == VE_CONVERGED;
+    r.extrapolated = q.ve_mode == VE_EXTRAPOLATE && post[b].ncycles == 1;
+    if (q.ve_mode == VE_EXTRAPOLATE) {
+      r.kappa_used = q.ve_k;
+      r.method = q.ve_method;
+      r.fallback = q.ve_fallback;
+      r.stability_sum = q.ve_stab;
+      for (int i = 0; i <= q.ve_k && i < 12; ++i) {
+        r.gamma[i] = q.ve_gamma[i];
+        r.c[i] = q.ve_c[i];
+      }
+    }
+  }
+  return REDVE_OK;
+}
+
+}  // extern "C"

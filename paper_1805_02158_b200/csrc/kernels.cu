@@ -1,0 +1,915 @@
+// RED fixed-point / vector-extrapolation kernels for B200 (sm_100a), fp64.
+//
+// Fourier fixed-point step  x+ = x_b + IDFT( alpha/(d HW) * DFT f(x) ),
+// d = |H^|^2/sigma^2 + alpha, x_b = IDFT(DFT(H^T y/sigma^2)/d)
+// (objective.py:100-104; the split is exact algebra: the step is linear in
+// its right-hand side).  Two images of the batch ride as one complex image
+// (re = image 2p, im = image 2p+1): the spectral multiplier is real and
+// even, so the complex transform of the pair yields both real results.
+//
+//   k_row_fwd : tile (+halo) -> fused denoiser -> row FFTs        -> Z
+//   k_col     : Z columns -> FFT -> * alpha g -> inverse FFT        -> Z
+//   k_row_inv : Z rows -> inverse FFT -> + x_b -> x+  (+ step-norm record)
+//
+// Per-image reductions are deterministic: per-CTA partials, then the last
+// CTA of the image (atomic ticket) sums them in CTA order.
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace redve {
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+
+__global__ void k_row_fwd(RowFwdArgs a);
+__global__ void k_col(ColArgs a);
+__global__ void k_row_inv(RowInvArgs a);
+__global__ void k_cost(CostArgs a);
+
+static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// --------------------------------------------------------------- setup
+void configure_kernels() {
+  const int big = 227 * 1024;
+  cudaFuncSetAttribute(k_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
+__global__ void k_twiddles(cd* tw, int L) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < L) {
+    double s, c;
+    sincospi(2.0 * (double)m / (double)L, &s, &c);
+    tw[m] = cd{c, s};
+  }
+}
+void launch_twiddles(cd* tw, int L, cudaStream_t s) {
+  k_twiddles<<<cdiv(L, 256), 256, 0, s>>>(tw, L);
+}
+
+// g[k1][k2] = 1 / ((|H^(k1,k2)|^2/sigma^2 + alpha) * H * W)   (objective.py:71-72)
+// H^ = sum taps[a][b] exp(-2 pi i (k1 (a-r)/H + k2 (b-r)/W))   (imaging.py:113-129)
+__global__ void k_inv_denom(double* g, int H, int W, const double* taps, int hk, double sigma,
+                            double alpha) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= H * W) return;
+  int k1 = idx / W, k2 = idx % W;
+  int r = hk / 2;
+  double re = 0.0, im = 0.0;
+  for (int a = 0; a < hk; ++a) {
+    long long pa = ((long long)k1 * (a - r)) % H;
+    if (pa < 0) pa += H;
+    for (int b = 0; b < hk; ++b) {
+      long long pb = ((long long)k2 * (b - r)) % W;
+      if (pb < 0) pb += W;
+      double ph = (double)pa / H + (double)pb / W;  // in turns
+      double s, c;
+      sincospi(2.0 * ph, &s, &c);
+      double t = taps[a * hk + b];
+      re += t * c;
+      im -= t * s;
+    }
+  }
+  double d = (re * re + im * im) / (sigma * sigma) + alpha;
+  g[idx] = 1.0 / (d * (double)H * (double)W);
+}
+void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, double sigma,
+                      double alpha, cudaStream_t s) {
+  k_inv_denom<<<cdiv((long long)H * W, 128), 128, 0, s>>>(g, H, W, taps, hk, sigma, alpha);
+}
+
+// --------------------------------------------------------------- smem plans
+static inline __host__ __device__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+size_t row_fwd_smem(int W, int lpc, int radius, int ksize) {
+  size_t tile = (size_t)(lpc + 2 * radius) * W * sizeof(cd);
+  size_t lines = (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd);
+  return al16(W * sizeof(cd)) + al16((size_t)ksize * ksize * sizeof(double)) +
+         (tile > lines ? tile : lines);
+}
+size_t col_smem(int H, int lpc) { return al16(H * sizeof(cd)) + (size_t)H * lpc * sizeof(cd); }
+size_t row_inv_smem(int W, int lpc) {
+  return al16(W * sizeof(cd)) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
+         al16(32 * 6 * sizeof(double));
+}
+
+// --------------------------------------------------------------- row forward
+__global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const bool a0 = takes_step(a.st[b0], a.phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
+  if (!a0 && !a1) return;
+  const int W = a.W, H = a.H, T = threads_per_line(W), R = a.dn.radius;
+  const int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  cd* s_tw = reinterpret_cast<cd*>(g_smem);
+  double* s_taps = reinterpret_cast<double*>(g_smem + al16(W * sizeof(cd)));
+  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(W * sizeof(cd)) +
+                                     al16((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
+  load_twiddles(s_tw, a.tw, W);
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) s_taps[i] = a.dn.taps[i];
+  const double* x0 = a0 ? a.xin.at(b0, a.st) : nullptr;
+  const double* x1 = a1 ? a.xin.at(b1, a.st) : nullptr;
+  const int r0 = blockIdx.x * a.lpc;
+  const int trows = a.lpc + 2 * R;
+  for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
+    int i = idx / W, c = idx - i * W;
+    int gr = wrap(r0 - R + i, H);
+    long long o = (long long)gr * W + c;
+    st_cd(s_work + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+  }
+  __syncthreads();
+  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
+  const int row = r0 + line;
+  const bool valid = row < H;
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int c = t + T * m;
+    v[m] = (valid && c < W) ? denoise_at(s_work, W, line + R, c, a.dn.kind, a.dn.ksize, s_taps)
+                            : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  RowLayout lay{RowLayout::stride_for(W)};
+  line_fft<false>(v, s_work, s_tw, W, t, line, lay);
+  if (valid) {
+    cd* zr = a.Z + ((long long)p * H + row) * W;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      int c = t + T * m;
+      if (c < W) st_cd(zr + c, v[m]);
+    }
+  }
+}
+void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s) {
+  int T = threads_per_line(a.W);
+  size_t sm = row_fwd_smem(a.W, a.lpc, a.dn.radius, a.dn.ksize);
+  dim3 grid(cdiv(a.H, a.lpc), npairs);
+  k_row_fwd<<<grid, a.lpc * T, sm, s>>>(a);
+}
+
+// --------------------------------------------------------------- columns
+__global__ void __launch_bounds__(256) k_col(ColArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const bool a0 = takes_step(a.st[b0], a.phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
+  if (!a0 && !a1) return;
+  const int H = a.H, W = a.W, T = threads_per_line(H);
+  cd* s_tw = reinterpret_cast<cd*>(g_smem);
+  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(H * sizeof(cd)));
+  load_twiddles(s_tw, a.tw, H);
+  const int line = threadIdx.x % a.lpc, t = threadIdx.x / a.lpc;
+  const int col = blockIdx.x * a.lpc + line;
+  const bool valid = col < W;
+  cd* zc = a.Z + (long long)p * H * W + col;
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int r = t + T * m;
+    v[m] = (valid && r < H) ? ld_cd(zc + (long long)r * W) : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  ColLayout lay{a.lpc};
+  line_fft<false>(v, s_work, s_tw, H, t, line, lay);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int r = t + T * m;
+    if (valid && r < H) v[m] = v[m] * (a.scale * __ldg(a.g + (long long)r * W + col));
+  }
+  line_fft<true>(v, s_work, s_tw, H, t, line, lay);
+  if (valid) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      int r = t + T * m;
+      if (r < H) st_cd(zc + (long long)r * W, v[m]);
+    }
+  }
+}
+void launch_col(const ColArgs& a, int npairs, cudaStream_t s) {
+  int T = threads_per_line(a.H);
+  dim3 grid(cdiv(a.W, a.lpc), npairs);
+  k_col<<<grid, a.lpc * T, col_smem(a.H, a.lpc), s>>>(a);
+}
+
+// --------------------------------------------------------------- record
+// solvers.py:225-253 (_Recorder.record) minus the cost/psnr part (k_cost).
+__device__ void record_step(ImgState& s, int b, double d2, double x2, double nf, int S,
+                            const StepCtl& ctl, const TraceBufs& tr) {
+  s.stepped = 1;
+  s.k += 1;
+  s.cur = (s.cur + 1) % S;
+  double den = sqrt(x2);
+  if (den == 0.0) den = 1.0;
+  const double sn = sqrt(d2) / den;
+  const long long i = (long long)b * tr.cap + (s.k - 1);
+  if (s.k - 1 < tr.cap) {
+    tr.step_norm[i] = sn;
+    tr.elapsed[i] = (double)(globaltimer_ns() - s.t0) * 1e-9;
+  }
+  if (nf > 0.0) s.err = ERR_NONFINITE_X;
+  s.pending = RUNNING;
+  if (ctl.phase == PH_MAIN) {
+    if (sn <= ctl.tol) s.pending = CONVERGED;
+    else if (s.k >= ctl.budget) s.pending = BUDGET;
+  }
+  if (!ctl.defer_commit) commit_step(s, ctl.phase);
+}
+
+// --------------------------------------------------------------- row inverse
+__global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
+  const bool a0 = takes_step(a.st[b0], phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
+  if (!a0 && !a1) return;
+  const int W = a.W, H = a.H, T = threads_per_line(W);
+  const long long N = (long long)H * W;
+  cd* s_tw = reinterpret_cast<cd*>(g_smem);
+  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(W * sizeof(cd)));
+  double* s_red = reinterpret_cast<double*>(g_smem + al16(W * sizeof(cd)) +
+                                            (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
+  load_twiddles(s_tw, a.tw, W);
+  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
+  const int row = blockIdx.x * a.lpc + line;
+  const bool valid = row < H;
+  const cd* zr = a.Z + ((long long)p * H + (valid ? row : 0)) * W;
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int c = t + T * m;
+    v[m] = (valid && c < W) ? ld_cd(zr + c) : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  RowLayout lay{RowLayout::stride_for(W)};
+  line_fft<true>(v, s_work, s_tw, W, t, line, lay);
+
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  if (valid) {
+    double* o0 = a0 ? a.out.at(b0, a.st) : nullptr;
+    double* o1 = a1 ? a.out.at(b1, a.st) : nullptr;
+    const double* p0 = (a0 && a.epilogue) ? a.xprev.at(b0, a.st) : nullptr;
+    const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) : nullptr;
+    const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N : nullptr;
+    const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N : nullptr;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      int c = t + T * m;
+      if (c >= W) continue;
+      long long o = (long long)row * W + c;
+      if (o0) {
+        double val = v[m].x + (bs0 ? __ldg(bs0 + o) : 0.0);
+        o0[o] = val;
+        if (p0) {
+          double xp = __ldg(p0 + o), d = val - xp;
+          acc[0] = fma(d, d, acc[0]);
+          acc[1] = fma(xp, xp, acc[1]);
+          acc[2] += isfinite(val) ? 0.0 : 1.0;
+        }
+      }
+      if (o1) {
+        double val = v[m].y + (bs1 ? __ldg(bs1 + o) : 0.0);
+        o1[o] = val;
+        if (p1) {
+          double xp = __ldg(p1 + o), d = val - xp;
+          acc[3] = fma(d, d, acc[3]);
+          acc[4] = fma(xp, xp, acc[4]);
+          acc[5] += isfinite(val) ? 0.0 : 1.0;
+        }
+      }
+    }
+  }
+  if (!a.epilogue) return;
+  block_sum<6>(acc, s_red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) {
+    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (int blk = 0; blk < nblk; ++blk) {
+      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
+      for (int i = 0; i < 6; ++i) tot[i] += src[i];
+    }
+    if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
+    if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
+  }
+}
+void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s) {
+  int T = threads_per_line(a.W);
+  dim3 grid(cdiv(a.H, a.lpc), npairs);
+  k_row_inv<<<grid, a.lpc * T, row_inv_smem(a.W, a.lpc), s>>>(a);
+}
+
+// --------------------------------------------------------------- cost
+// E(x) = ||Hx - y||^2/(2 sigma^2) + alpha/2 x.(x - f(x))   (objective.py:78-88)
+// PSNR = 10 log10(255^2 / mse)                          (imaging.py:234-248)
+// Modes: record on the logging cadence (solvers.py:232-238, best-iterate
+// tracking :235-236), note_initial (:219-223), finalize (:255-262).
+__device__ double psnr_from(double ssd, long long n) {
+  double mse = ssd / (double)n;
+  if (mse == 0.0) return INFINITY;
+  if (!isfinite(mse)) return -INFINITY;
+  return 10.0 * log10(255.0 * 255.0 / mse);
+}
+
+__device__ void cost_finish(ImgState& s, int b, double fid, double reg, double ssd, bool has_ref,
+                            const CostArgs& a) {
+  const double cost = fid / (2.0 * a.sigma * a.sigma) + a.alpha * (0.5 * reg);
+  const long long N = (long long)a.H * a.W;
+  if (a.mode == COST_INIT) {
+    if (isfinite(cost)) {
+      s.best_cost = cost;
+      s.copy_best = 1;
+      s.has_best = 1;
+    } else {
+      s.copy_best = 0;
+    }
+    return;
+  }
+  if (a.mode == COST_FINAL) {
+    s.use_best = (s.has_best && !(isfinite(cost) && cost <= s.best_cost)) ? 1 : 0;
+    return;
+  }
+  const long long i = (long long)b * a.tr.cap + (s.k - 1);
+  if (s.k - 1 < a.tr.cap) {
+    a.tr.cost[i] = cost;
+    if (has_ref) a.tr.psnr[i] = psnr_from(ssd, N);
+  }
+  s.copy_best = 0;
+  if (a.ctl.track_best && cost < s.best_cost) {
+    s.best_cost = cost;
+    s.copy_best = 1;
+    s.has_best = 1;
+  }
+  if (!isfinite(cost) && s.err == ERR_NONE) s.err = ERR_NONFINITE_COST;
+}
+
+__device__ __forceinline__ bool cost_wants(const ImgState& s, const CostArgs& a) {
+  if (a.mode == COST_RECORD) return s.stepped && (s.k % a.ctl.log_every == 0);
+  if (a.mode == COST_INIT || a.mode == COST_VALUE) return true;
+  return s.err == ERR_NONE;  // final
+}
+
+__global__ void __launch_bounds__(256) k_cost(CostArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const bool has1 = b1 < a.B;
+  const bool w0 = cost_wants(a.st[b0], a);
+  const bool w1 = has1 && cost_wants(a.st[b1], a);
+  const int nblk = gridDim.x;
+  if (!w0 && !w1) {
+    // nothing to evaluate; block 0 still commits the step for stepped images
+    if (a.mode == COST_RECORD && blockIdx.x == 0 && threadIdx.x == 0) {
+      commit_step(a.st[b0], a.ctl.phase);
+      if (has1) commit_step(a.st[b1], a.ctl.phase);
+    }
+    return;
+  }
+  const int W = a.W, H = a.H;
+  const long long N = (long long)H * W;
+  const int rH = a.hk / 2;
+  const int R = max(rH, a.dn.kind == DN_EXTERNAL ? 0 : a.dn.radius);
+  const int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  double* s_h = reinterpret_cast<double*>(g_smem);
+  double* s_taps = s_h + a.hk * a.hk;
+  double* s_red = s_taps + kk;
+  cd* tile = reinterpret_cast<cd*>(g_smem + al16((a.hk * a.hk + kk + 32 * 3 * 2) * sizeof(double)));
+  for (int i = threadIdx.x; i < a.hk * a.hk; i += blockDim.x) s_h[i] = a.htaps[i];
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) s_taps[i] = a.dn.taps[i];
+  const double* x0 = w0 ? a.x.at(b0, a.st) : nullptr;
+  const double* x1 = w1 ? a.x.at(b1, a.st) : nullptr;
+  const int r0 = blockIdx.x * a.rows;
+  const int trows = a.rows + 2 * R;
+  for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
+    int i = idx / W, c = idx - i * W;
+    int gr = wrap(r0 - R + i, H);
+    long long o = (long long)gr * W + c;
+    st_cd(tile + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+  }
+  __syncthreads();
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // fid0, reg0, ssd0, fid1, reg1, ssd1
+  const int s = a.factor;
+  for (int idx = threadIdx.x; idx < a.rows * W; idx += blockDim.x) {
+    const int li = idx / W, c = idx - li * W;
+    const int row = r0 + li;
+    if (row >= H) break;
+    const long long o = (long long)row * W + c;
+    const cd xv = ld_cd(tile + (li + R) * W + c);
+    cd fv;
+    if (a.dn.kind == DN_EXTERNAL) {
+      fv = cd{x0 ? __ldg(a.fext + (long long)b0 * N + o) : 0.0,
+              x1 ? __ldg(a.fext + (long long)b1 * N + o) : 0.0};
+    } else {
+      fv = denoise_at(tile, W, li + R, c, a.dn.kind, a.dn.ksize, s_taps);
+    }
+    acc[1] = fma(xv.x, xv.x - fv.x, acc[1]);
+    acc[4] = fma(xv.y, xv.y - fv.y, acc[4]);
+    if (a.ref) {
+      if (x0) {
+        double d = xv.x - __ldg(a.ref + (long long)b0 * N + o);
+        acc[2] = fma(d, d, acc[2]);
+      }
+      if (x1) {
+        double d = xv.y - __ldg(a.ref + (long long)b1 * N + o);
+        acc[5] = fma(d, d, acc[5]);
+      }
+    }
+    if ((row % s) == 0 && (c % s) == 0) {
+      // (H x)(row, c) = sum taps[a][b] x[row-(a-r), c-(b-r)], then - y
+      cd hx = cd{0.0, 0.0};
+      for (int ta = 0; ta < a.hk; ++ta) {
+        const cd* trow = tile + (li + R - (ta - rH)) * W;
+        for (int tb = 0; tb < a.hk; ++tb) {
+          const double w = s_h[ta * a.hk + tb];
+          cd xx = ld_cd(trow + wrap(c - (tb - rH), W));
+          hx.x = fma(w, xx.x, hx.x);
+          hx.y = fma(w, xx.y, hx.y);
+        }
+      }
+      const long long oy = (long long)(row / s) * a.Wy + (c / s);
+      const long long Ny = (long long)a.Hy * a.Wy;
+      if (x0) {
+        double d = hx.x - __ldg(a.y + (long long)b0 * Ny + oy);
+        acc[0] = fma(d, d, acc[0]);
+      }
+      if (x1) {
+        double d = hx.y - __ldg(a.y + (long long)b1 * Ny + oy);
+        acc[3] = fma(d, d, acc[3]);
+      }
+    }
+  }
+  block_sum<6>(acc, s_red);
+  if (threadIdx.x == 0) {
+    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
+    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (int blk = 0; blk < nblk; ++blk) {
+      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
+      for (int i = 0; i < 6; ++i) tot[i] += src[i];
+    }
+    if (a.mode == COST_VALUE) {
+      for (int i = 0; i < 3; ++i) {
+        a.out_vals[b0 * 3 + i] = tot[i];
+        if (has1) a.out_vals[b1 * 3 + i] = tot[3 + i];
+      }
+    } else {
+      if (w0) cost_finish(a.st[b0], b0, tot[0], tot[1], tot[2], a.ref != nullptr, a);
+      if (w1) cost_finish(a.st[b1], b1, tot[3], tot[4], tot[5], a.ref != nullptr, a);
+    }
+    if (a.mode == COST_RECORD) {
+      commit_step(a.st[b0], a.ctl.phase);
+      if (has1) commit_step(a.st[b1], a.ctl.phase);
+    }
+  }
+}
+int cost_rows(int H) { return H < 8 ? H : 8; }
+void launch_cost(const CostArgs& a, int npairs, cudaStream_t s) {
+  int R = max(a.hk / 2, a.dn.kind == DN_EXTERNAL ? 0 : a.dn.radius);
+  int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  size_t sm = al16((a.hk * a.hk + kk + 32 * 3 * 2) * sizeof(double)) +
+              (size_t)(a.rows + 2 * R) * a.W * sizeof(cd);
+  dim3 grid(cdiv(a.H, a.rows), npairs);
+  k_cost<<<grid, 256, sm, s>>>(a);
+}
+
+// --------------------------------------------------------------- copies
+__global__ void k_copy_view(View dst, View src, int B, long long N, const ImgState* st,
+                            int only_flag) {
+  const int b = blockIdx.y;
+  if (only_flag && !st[b].copy_best) return;
+  double* d = dst.at(b, st);
+  const double* s = src.at(b, st);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
+                      cudaStream_t s) {
+  int chunks = cdiv(N, 256 * 8);
+  if (chunks > 64) chunks = 64;
+  k_copy_view<<<dim3(chunks, B), 256, 0, s>>>(dst, src, B, N, st, only_flag);
+}
+
+__global__ void k_gather(double* out, View cur, const double* best, int B, long long N,
+                         const ImgState* st) {
+  const int b = blockIdx.y;
+  const double* s = st[b].use_best ? best + (long long)b * N : cur.at(b, st);
+  double* d = out + (long long)b * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+void launch_gather(double* out, View cur, const double* best, int B, long long N,
+                   const ImgState* st, cudaStream_t s) {
+  int chunks = cdiv(N, 256 * 8);
+  if (chunks > 64) chunks = 64;
+  k_gather<<<dim3(chunks, B), 256, 0, s>>>(out, cur, best, B, N, st);
+}
+
+__global__ void k_init_state(ImgState* st, int B) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ImgState s;
+  memset(&s, 0, sizeof(s));
+  s.best_cost = INFINITY;
+  s.t0 = globaltimer_ns();
+  st[b] = s;
+}
+void launch_init_state(ImgState* st, int B, cudaStream_t s) {
+  k_init_state<<<cdiv(B, 128), 128, 0, s>>>(st, B);
+}
+
+// --------------------------------------------------------------- VE: Gram
+__device__ __forceinline__ bool ve_participates(const ImgState& s) {
+  return s.term == RUNNING || s.term == BUDGET;
+}
+__device__ __forceinline__ const double* slot_ptr(const VeArgs& a, int b, int slot) {
+  return a.ring + (long long)b * a.img_stride + (long long)(slot % a.S) * a.slot_stride;
+}
+
+template <int KP1>
+__global__ void __launch_bounds__(256) k_gram(VeArgs a) {
+  constexpr int NG = KP1 * (KP1 + 1) / 2;
+  const int b = blockIdx.y;
+  ImgState& s = a.st[b];
+  if (!ve_participates(s)) return;
+  __shared__ double s_red[32 * NG];
+  const double* w[KP1 + 1];
+  const int s0 = s.start + a.m;
+#pragma unroll
+  for (int j = 0; j <= KP1; ++j) w[j] = slot_ptr(a, b, s0 + j);
+  double acc[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) acc[i] = 0.0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
+       p += (long long)gridDim.x * blockDim.x) {
+    double d[KP1];
+    double prev = __ldg(w[0] + p);
+#pragma unroll
+    for (int j = 0; j < KP1; ++j) {
+      double nx = __ldg(w[j + 1] + p);
+      d[j] = nx - prev;
+      prev = nx;
+    }
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < KP1; ++i)
+#pragma unroll
+      for (int j = i; j < KP1; ++j) {
+        acc[q] = fma(d[i], d[j], acc[q]);
+        ++q;
+      }
+  }
+  block_sum<NG>(acc, s_red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) {
+    double* dst = a.partials + ((long long)b * nblk + blockIdx.x) * NG;
+    for (int i = 0; i < NG; ++i) dst[i] = acc[i];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double G[KP1 * KP1];
+    double tot[NG];
+    for (int i = 0; i < NG; ++i) tot[i] = 0.0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const volatile double* src = a.partials + ((long long)b * nblk + blk) * NG;
+      for (int i = 0; i < NG; ++i) tot[i] += src[i];
+    }
+    int q = 0;
+    for (int i = 0; i < KP1; ++i)
+      for (int j = i; j < KP1; ++j) {
+        G[i * KP1 + j] = tot[q];
+        G[j * KP1 + i] = tot[q];
+        ++q;
+      }
+    VeOut o;
+    decide_from_gram(G, KP1, a.method, a.rank_tol, o);
+    s.ve_mode = o.mode;
+    if (o.mode == VE_EXTRAPOLATE) {
+      s.ve_k = o.k_used;
+      s.ve_method = o.method;
+      s.ve_fallback = o.fallback;
+      s.ve_stab = o.stab;
+      for (int i = 0; i <= o.k_used; ++i) {
+        s.ve_gamma[i] = o.gamma[i];
+        s.ve_c[i] = o.c[i];
+        if (i < o.k_used) s.ve_xi[i] = o.xi[i];
+      }
+    }
+  }
+}
+
+template <int KP1>
+static void launch_gram_t(const VeArgs& a, cudaStream_t s) {
+  k_gram<KP1><<<dim3(a.chunks, a.B), 256, 0, s>>>(a);
+}
+void launch_gram(const VeArgs& a, cudaStream_t s) {
+  switch (a.kp1) {
+    case 2: launch_gram_t<2>(a, s); break;
+    case 3: launch_gram_t<3>(a, s); break;
+    case 4: launch_gram_t<4>(a, s); break;
+    case 5: launch_gram_t<5>(a, s); break;
+    case 6: launch_gram_t<6>(a, s); break;
+    case 7: launch_gram_t<7>(a, s); break;
+    case 8: launch_gram_t<8>(a, s); break;
+    case 9: launch_gram_t<9>(a, s); break;
+    case 10: launch_gram_t<10>(a, s); break;
+    case 11: launch_gram_t<11>(a, s); break;
+    default: launch_gram_t<12>(a, s); break;
+  }
+}
+
+// --------------------------------------------------------------- VE: exact MGS route
+// mgs_qr (extrapolation.py:159-196) for the rare windows whose rank question
+// the Gram route cannot resolve.  One CTA per flagged image.
+__device__ double block_dot(const double* u, const double* v, long long N, double* s_red) {
+  double acc[1] = {0.0};
+  for (long long p = threadIdx.x; p < N; p += blockDim.x) acc[0] = fma(u[p], v[p], acc[0]);
+  block_sum<1>(acc, s_red);
+  __shared__ double s_bc;
+  if (threadIdx.x == 0) s_bc = acc[0];
+  __syncthreads();
+  return s_bc;
+}
+
+__global__ void __launch_bounds__(512) k_mgs(VeArgs a) {
+  const int b = blockIdx.x;
+  ImgState& s = a.st[b];
+  if (!ve_participates(s) || s.ve_mode != VE_MGS) return;
+  __shared__ double s_red[32];
+  __shared__ double R[MAXKP1][MAXKP1];
+  __shared__ int s_stop;
+  const int n = a.kp1;
+  const long long N = a.N;
+  double* Q = a.qscratch + (long long)b * n * N;
+  if (threadIdx.x < MAXKP1 * MAXKP1) (&R[0][0])[threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) s_stop = 0;
+  __syncthreads();
+  const int s0 = s.start + a.m;
+  int rank = n;
+  double r11 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double* xa = slot_ptr(a, b, s0 + i);
+    const double* xb = slot_ptr(a, b, s0 + i + 1);
+    double* qi = Q + (long long)i * N;
+    for (long long p = threadIdx.x; p < N; p += blockDim.x) qi[p] = xb[p] - xa[p];
+    __syncthreads();
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (int j = 0; j < i; ++j) {
+        const double* qj = Q + (long long)j * N;
+        double proj = block_dot(qj, qi, N, s_red);
+        if (threadIdx.x == 0) R[j][i] += proj;
+        for (long long p = threadIdx.x; p < N; p += blockDim.x) qi[p] -= proj * qj[p];
+        __syncthreads();
+      }
+    }
+    double rii = sqrt(block_dot(qi, qi, N, s_red));
+    if (threadIdx.x == 0) R[i][i] = rii;
+    if (i == 0) {
+      if (rii < 1e-300) {
+        if (threadIdx.x == 0) s.ve_mode = VE_CONVERGED;
+        return;
+      }
+      r11 = rii;
+    } else if (rii < a.rank_tol * r11) {
+      rank = i;
+      break;
+    }
+    for (long long p = threadIdx.x; p < N; p += blockDim.x) qi[p] /= rii;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bool finite = true;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) finite = finite && isfinite(R[i][j]);
+    VeOut o;
+    if (!finite) {
+      o.mode = VE_SKIP;
+    } else {
+      decide_from_r(R, n, rank, a.method, o);
+    }
+    s.ve_mode = o.mode;
+    if (o.mode == VE_EXTRAPOLATE) {
+      s.ve_k = o.k_used;
+      s.ve_method = o.method;
+      s.ve_fallback = o.fallback;
+      s.ve_stab = o.stab;
+      for (int i = 0; i <= o.k_used; ++i) {
+        s.ve_gamma[i] = o.gamma[i];
+        s.ve_c[i] = o.c[i];
+        if (i < o.k_used) s.ve_xi[i] = o.xi[i];
+      }
+    }
+  }
+}
+void launch_mgs(const VeArgs& a, cudaStream_t s) { k_mgs<<<a.B, 512, 0, s>>>(a); }
+
+// --------------------------------------------------------------- VE: combine
+// x = x_m + sum_{j<k} xi_j (x_{m+j+1} - x_{m+j})  written over the cycle-start
+// slot; accepted only if finite (solvers.py:368-378).
+__global__ void __launch_bounds__(256) k_combine(VeArgs a) {
+  const int b = blockIdx.y;
+  ImgState& s = a.st[b];
+  if (!ve_participates(s)) return;
+  const int mode = s.ve_mode;
+  if (mode != VE_EXTRAPOLATE) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (mode == VE_CONVERGED) {
+        s.cur = (s.start + a.m) % a.S;
+        s.term = CONVERGED;
+      }
+      s.start = s.cur;
+    }
+    return;
+  }
+  __shared__ double s_xi[MAXKP1];
+  __shared__ double s_red[32];
+  const int ke = s.ve_k;
+  if (threadIdx.x < ke) s_xi[threadIdx.x] = s.ve_xi[threadIdx.x];
+  __syncthreads();
+  const int s0 = s.start + a.m;
+  const double* w[MAXKP1 + 1];
+  for (int j = 0; j <= ke; ++j) w[j] = slot_ptr(a, b, s0 + j);
+  double* out = a.ring + (long long)b * a.img_stride + (long long)s.start * a.slot_stride;
+  double nf[1] = {0.0};
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
+       p += (long long)gridDim.x * blockDim.x) {
+    double prev = w[0][p];
+    double acc = prev;
+    for (int j = 0; j < ke; ++j) {
+      double nx = w[j + 1][p];
+      acc = fma(s_xi[j], nx - prev, acc);
+      prev = nx;
+    }
+    out[p] = acc;
+    nf[0] += isfinite(acc) ? 0.0 : 1.0;
+  }
+  block_sum<1>(nf, s_red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) a.partials[(long long)b * nblk + blockIdx.x] = nf[0];
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int blk = 0; blk < nblk; ++blk)
+      tot += ((volatile double*)a.partials)[(long long)b * nblk + blk];
+    if (tot == 0.0) {
+      s.cur = s.start;
+      const TraceBufs& tr = a.tr;
+      if (s.k - 1 < tr.cap) tr.gamma[(long long)b * tr.cap + s.k - 1] = s.ve_stab;
+      if (s.ncycles < tr.ccap) {
+        long long c = (long long)b * tr.ccap + s.ncycles;
+        tr.cyc_meta[c * 4 + 0] = s.ve_method;
+        tr.cyc_meta[c * 4 + 1] = s.ve_fallback;
+        tr.cyc_meta[c * 4 + 2] = ke;
+        tr.cyc_meta[c * 4 + 3] = s.k - 1;
+        tr.cyc_stab[c] = s.ve_stab;
+        for (int i = 0; i < MAXKP1; ++i) {
+          tr.cyc_gamma[c * MAXKP1 + i] = i <= ke ? s.ve_gamma[i] : 0.0;
+          tr.cyc_c[c * MAXKP1 + i] = i <= ke ? s.ve_c[i] : 0.0;
+        }
+      }
+      s.ncycles += 1;
+    }
+    // else: discard the cycle, continue from the last plain iterate (cur)
+    s.start = s.cur;
+  }
+}
+void launch_combine(const VeArgs& a, cudaStream_t s) {
+  k_combine<<<dim3(a.chunks, a.B), 256, 0, s>>>(a);
+}
+
+// --------------------------------------------------------------- stencils (operator API)
+// out = scale * (conv or corr)(x, taps), periodic   (imaging.py:132-170)
+__global__ void k_conv(const double* x, double* out, int B, int H, int W, const double* taps,
+                       int k, int corr, double scale) {
+  const long long N = (long long)H * W;
+  const int r = k / 2;
+  const int b = blockIdx.y;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+    double acc = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int c = 0; c < k; ++c) {
+        int di = corr ? (a - r) : -(a - r);
+        int dj = corr ? (c - r) : -(c - r);
+        acc = fma(taps[a * k + c], __ldg(x + (long long)b * N + (long long)wrap(i + di, H) * W +
+                                             wrap(j + dj, W)),
+                  acc);
+      }
+    out[(long long)b * N + idx] = scale * acc;
+  }
+}
+void launch_conv(const double* x, double* out, int B, int H, int W, const double* taps, int k,
+                 int corr, double scale, cudaStream_t s) {
+  long long N = (long long)H * W;
+  int chunks = cdiv(N, 256);
+  if (chunks > 1024) chunks = 1024;
+  k_conv<<<dim3(chunks, B), 256, 0, s>>>(x, out, B, H, W, taps, k, corr, scale);
+}
+
+// BlurDownsample.apply: conv, keep indices == 0 mod s   (imaging.py:193-197)
+__global__ void k_decimate_conv(const double* x, double* out, int B, int H, int W, int f,
+                                const double* taps, int k) {
+  const int Hy = (H + f - 1) / f, Wy = (W + f - 1) / f;
+  const long long Ny = (long long)Hy * Wy, N = (long long)H * W;
+  const int r = k / 2, b = blockIdx.y;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < Ny;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / Wy) * f, j = (int)(idx % Wy) * f;
+    double acc = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int c = 0; c < k; ++c)
+        acc = fma(taps[a * k + c],
+                  __ldg(x + (long long)b * N + (long long)wrap(i - (a - r), H) * W +
+                        wrap(j - (c - r), W)),
+                  acc);
+    out[(long long)b * Ny + idx] = acc;
+  }
+}
+void launch_decimate_conv(const double* x, double* out, int B, int H, int W, int factor,
+                          const double* taps, int k, cudaStream_t s) {
+  long long Ny = (long long)((H + factor - 1) / factor) * ((W + factor - 1) / factor);
+  int chunks = cdiv(Ny, 256);
+  if (chunks > 1024) chunks = 1024;
+  k_decimate_conv<<<dim3(chunks, B), 256, 0, s>>>(x, out, B, H, W, factor, taps, k);
+}
+
+// BlurDownsample.adjoint: zero-fill then correlate   (imaging.py:199-204)
+__global__ void k_upsample_corr(const double* z, double* out, int B, int H, int W, int f,
+                                const double* taps, int k, double scale) {
+  const int Hy = (H + f - 1) / f, Wy = (W + f - 1) / f;
+  const long long Ny = (long long)Hy * Wy, N = (long long)H * W;
+  const int r = k / 2, b = blockIdx.y;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+    double acc = 0.0;
+    for (int a = 0; a < k; ++a) {
+      int u = wrap(i + (a - r), H);
+      if (u % f) continue;
+      for (int c = 0; c < k; ++c) {
+        int v = wrap(j + (c - r), W);
+        if (v % f) continue;
+        acc = fma(taps[a * k + c], __ldg(z + (long long)b * Ny + (long long)(u / f) * Wy + v / f),
+                  acc);
+      }
+    }
+    out[(long long)b * N + idx] = scale * acc;
+  }
+}
+void launch_upsample_corr(const double* z, double* out, int B, int H, int W, int factor,
+                          const double* taps, int k, double scale, cudaStream_t s) {
+  long long N = (long long)H * W;
+  int chunks = cdiv(N, 256);
+  if (chunks > 1024) chunks = 1024;
+  k_upsample_corr<<<dim3(chunks, B), 256, 0, s>>>(z, out, B, H, W, factor, taps, k, scale);
+}
+
+__global__ void k_median3(const double* x, double* out, int B, int H, int W) {
+  const long long N = (long long)H * W;
+  const int b = blockIdx.y;
+  const double* xb = x + (long long)b * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+    double v[9];
+    int q = 0;
+    for (int a = -1; a <= 1; ++a)
+      for (int c = -1; c <= 1; ++c)
+        v[q++] = __ldg(xb + (long long)wrap(i + a, H) * W + wrap(j + c, W));
+    out[(long long)b * N + idx] = median9(v);
+  }
+}
+void launch_median3(const double* x, double* out, int B, int H, int W, cudaStream_t s) {
+  long long N = (long long)H * W;
+  int chunks = cdiv(N, 256);
+  if (chunks > 1024) chunks = 1024;
+  k_median3<<<dim3(chunks, B), 256, 0, s>>>(x, out, B, H, W);
+}
+
+}  // namespace redve
+
+namespace redve {
+// window-level extrapolate_once: the window is a ring of `S` = kappa+2 slots,
+// cycle start at slot 0, current iterate = last row.
+__global__ void k_window_setup(ImgState* st, int B, int S, int m) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  st[b].start = 0;
+  st[b].cur = S - 1;
+  st[b].k = 1;
+  st[b].term = RUNNING;
+  (void)m;
+}
+void launch_window_extrapolate_setup(ImgState* st, int B, int S, int m, cudaStream_t s) {
+  k_window_setup<<<cdiv(B, 128), 128, 0, s>>>(st, B, S, m);
+}
+}  // namespace redve

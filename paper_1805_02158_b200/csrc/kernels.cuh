@@ -1,0 +1,115 @@
+// Kernel argument blocks and launch helpers shared by kernels.cu and capi.cu.
+#pragma once
+
+#include "denoise.cuh"
+#include "fft.cuh"
+#include "state.cuh"
+#include "ve.cuh"
+
+namespace redve {
+
+struct RowFwdArgs {
+  int B, H, W, lpc;
+  View xin;
+  DenoiseArgs dn;
+  cd* Z;
+  const cd* tw;
+  const ImgState* st;
+  int phase;
+};
+
+struct ColArgs {
+  int B, H, W, lpc;
+  cd* Z;
+  const cd* tw;
+  const double* g;
+  double scale;
+  const ImgState* st;
+  int phase;
+};
+
+struct RowInvArgs {
+  int B, H, W, lpc;
+  const cd* Z;
+  const cd* tw;
+  View out;
+  const double* base;  // x_b [B][H*W] (added) or null
+  View xprev;          // epilogue: previous iterate
+  int epilogue;        // 1: record a fixed-point step
+  int S;
+  ImgState* st;
+  StepCtl ctl;
+  TraceBufs tr;
+  double* partials;
+  unsigned* counters;
+};
+
+enum CostMode : int { COST_RECORD = 0, COST_INIT = 1, COST_FINAL = 2, COST_VALUE = 3 };
+
+struct CostArgs {
+  int B, H, W, rows;  // rows per CTA
+  int Hy, Wy, factor;
+  View x;
+  const double* y;
+  const double* ref;
+  DenoiseArgs dn;
+  const double* fext;  // external f [B][N] (DN_EXTERNAL)
+  const double* htaps;
+  int hk;
+  double sigma, alpha;
+  int mode;
+  double* out_vals;  // COST_VALUE: [B][3] = ||Hx-y||^2, x.(x-f), ||x-ref||^2
+  ImgState* st;
+  StepCtl ctl;
+  TraceBufs tr;
+  double* partials;
+  unsigned* counters;
+};
+
+struct VeArgs {
+  int B;
+  long long N;
+  int m, kp1, S;
+  double* ring;
+  long long img_stride, slot_stride;
+  ImgState* st;
+  TraceBufs tr;
+  double* partials;
+  unsigned* counters;
+  double* qscratch;  // MGS [B][kp1][N]
+  int method;
+  double rank_tol;
+  int chunks;
+};
+
+// launchers (kernels.cu)
+void configure_kernels();
+void launch_twiddles(cd* tw, int L, cudaStream_t s);
+void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, double sigma,
+                      double alpha, cudaStream_t s);
+size_t row_fwd_smem(int W, int lpc, int radius, int ksize);
+size_t col_smem(int H, int lpc);
+size_t row_inv_smem(int W, int lpc);
+void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s);
+void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
+void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);
+int cost_rows(int H);
+void launch_cost(const CostArgs& a, int npairs, cudaStream_t s);
+void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
+                      cudaStream_t s);
+void launch_gram(const VeArgs& a, cudaStream_t s);
+void launch_mgs(const VeArgs& a, cudaStream_t s);
+void launch_combine(const VeArgs& a, cudaStream_t s);
+void launch_init_state(ImgState* st, int B, cudaStream_t s);
+void launch_gather(double* out, View cur, const double* best, int B, long long N,
+                   const ImgState* st, cudaStream_t s);
+void launch_conv(const double* x, double* out, int B, int H, int W, const double* taps, int k,
+                 int corr, double scale, cudaStream_t s);
+void launch_decimate_conv(const double* x, double* out, int B, int H, int W, int factor,
+                          const double* taps, int k, cudaStream_t s);
+void launch_upsample_corr(const double* z, double* out, int B, int H, int W, int factor,
+                          const double* taps, int k, double scale, cudaStream_t s);
+void launch_median3(const double* x, double* out, int B, int H, int W, cudaStream_t s);
+void launch_window_extrapolate_setup(ImgState* st, int B, int S, int m, cudaStream_t s);
+
+}  // namespace redve
