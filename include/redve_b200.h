@@ -138,6 +138,13 @@ const char* redve_last_error(const redve_ctx* ctx);
 int redve_set_stream(redve_ctx* ctx, void* cuda_stream); /* cudaStream_t, 0 = legacy default */
 int redve_synchronize(redve_ctx* ctx);
 const char* redve_version(void);
+/* total kernels this library has launched (all contexts) */
+uint64_t redve_kernel_launches(void);
+/* time every kernel with CUDA events on the context's stream (measurement aid) */
+int redve_profile(redve_ctx* ctx, int enable);
+/* per-kernel-kind totals since the last report: names is max_kinds x 32 chars */
+int redve_profile_report(redve_ctx* ctx, int max_kinds, char* names, double* total_ms,
+                         int64_t* count, int* n_kinds);
 
 /* ---- denoisers: f(x) for a batch (denoisers.py __call__) ------------------- */
 int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,

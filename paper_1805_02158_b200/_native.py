@@ -71,6 +71,10 @@ class VeResultC(C.Structure):
 # The exported symbols, exactly the declarations of include/redve_b200.h.
 SYMBOLS = {
     "redve_version": (C.c_char_p, []),
+    "redve_kernel_launches": (C.c_uint64, []),
+    "redve_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "redve_profile_report": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _dp, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int)]),
     "redve_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "redve_destroy": (None, [C.c_void_p]),
     "redve_last_error": (C.c_char_p, [C.c_void_p]),
@@ -168,3 +172,30 @@ def dptr(t):
 
 def hptr(a: np.ndarray, ctype=C.c_double):
     return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def profile(enable: bool, device: int | None = None):
+    lib = library()
+    lib.redve_profile(context(device), 1 if enable else 0)
+
+
+def profile_report(device: int | None = None):
+    """{kernel kind: (total_ms, launches)} since the last report (synchronises)."""
+    lib = library()
+    ctx = context(device)
+    mx = 64
+    names = C.create_string_buffer(32 * mx)
+    tot = np.zeros(mx)
+    cnt = np.zeros(mx, np.int64)
+    n = C.c_int()
+    check(lib.redve_profile_report(ctx, mx, names, hptr(tot), cnt.ctypes.data_as(
+        C.POINTER(C.c_int64)), C.byref(n)), ctx)
+    out = {}
+    for k in range(n.value):
+        nm = names.raw[32 * k: 32 * k + 32].split(b"\0")[0].decode()
+        out[nm] = (float(tot[k]), int(cnt[k]))
+    return out
+
+
+def kernel_launches() -> int:
+    return int(library().redve_kernel_launches())

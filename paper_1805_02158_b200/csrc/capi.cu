@@ -1,6 +1,7 @@
 // C ABI + native runtime: context, RED problem setup, device-resident solve
 // schedule (solvers.py:288-399 re-expressed as a static kernel schedule with
 // per-image masks), and the window-level VE entry point.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -35,7 +36,17 @@ struct DevBuf {
   }
 };
 
+static std::atomic<unsigned long long> g_launches{0};
+
+struct ProfEvent {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
 struct redve_ctx {
+  bool profiling = false;
+  std::vector<ProfEvent> prof;
+  std::vector<cudaEvent_t> ev_pool;
   int device = 0;
   cudaStream_t stream = 0;
   std::string err;
@@ -44,6 +55,21 @@ struct redve_ctx {
       ve_q, ve_trace;
   ~redve_ctx() {
     for (auto& kv : twiddles) delete kv.second;
+    for (auto& e : prof) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t ev() {
+    cudaEvent_t e;
+    if (!ev_pool.empty()) {
+      e = ev_pool.back();
+      ev_pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
   }
   const cd* tw(int L) {
     auto it = twiddles.find(L);
@@ -54,6 +80,7 @@ struct redve_ctx {
       return nullptr;
     }
     launch_twiddles(b->as<cd>(), L, stream);
+    g_launches.fetch_add(1);
     twiddles[L] = b;
     return b->as<cd>();
   }
@@ -74,6 +101,25 @@ static int fail(redve_ctx* c, int code, const char* fmt, ...) {
     cudaError_t e_ = (call);                                                        \
     if (e_ != cudaSuccess)                                                          \
       return fail(ctx, REDVE_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_));      \
+  } while (0)
+
+// Every kernel launch goes through RUN: counts it and, when profiling, brackets
+// it with CUDA events on the launching stream.
+#define RUN(ctx_, name_, call_)                                                     \
+  do {                                                                              \
+    redve_ctx* c_ = (ctx_);                                                         \
+    cudaEvent_t a_ = nullptr, b_ = nullptr;                                         \
+    if (c_ && c_->profiling) {                                                      \
+      a_ = c_->ev();                                                                \
+      b_ = c_->ev();                                                                \
+      cudaEventRecord(a_, c_->stream);                                              \
+    }                                                                               \
+    call_;                                                                          \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                             \
+    if (a_) {                                                                       \
+      cudaEventRecord(b_, c_->stream);                                              \
+      c_->prof.push_back(ProfEvent{name_, a_, b_});                                 \
+    }                                                                               \
   } while (0)
 
 #define CKL()                                                                       \
@@ -143,18 +189,18 @@ static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double s
   redve_ctx* ctx = p->ctx;
   RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, p->Z.as<cd>(), p->twW,
                 p->state.as<ImgState>(), phase};
-  launch_row_fwd(rf, p->npairs, ctx->stream);
+  RUN(ctx, "row_fwd", launch_row_fwd(rf, p->npairs, ctx->stream));
   CKL();
   ColArgs ca{p->B, p->H, p->W, p->lpc_col, p->Z.as<cd>(), p->twH, p->g.as<double>(), scale,
              p->state.as<ImgState>(), phase};
-  launch_col(ca, p->npairs, ctx->stream);
+  RUN(ctx, "col", launch_col(ca, p->npairs, ctx->stream));
   CKL();
   RowInvArgs ri;
   ri.B = p->B; ri.H = p->H; ri.W = p->W; ri.lpc = p->lpc_row;
   ri.Z = p->Z.as<cd>(); ri.tw = p->twW; ri.out = out; ri.base = base; ri.xprev = xprev;
   ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
   ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
-  launch_row_inv(ri, p->npairs, ctx->stream);
+  RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
   CKL();
   return REDVE_OK;
 }
@@ -173,6 +219,46 @@ extern "C" {
 
 const char* redve_version(void) { return "redve_b200 0.1.0 (sm_100a)"; }
 
+uint64_t redve_kernel_launches(void) { return g_launches.load(); }
+
+int redve_profile(redve_ctx* ctx, int enable) {
+  ctx->profiling = enable != 0;
+  return REDVE_OK;
+}
+
+int redve_profile_report(redve_ctx* ctx, int max_kinds, char* names, double* total_ms,
+                         int64_t* count, int* n_kinds) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<std::string> kinds;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& e : ctx->prof) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    size_t k = 0;
+    while (k < kinds.size() && kinds[k] != e.name) ++k;
+    if (k == kinds.size()) {
+      kinds.push_back(e.name);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += ms;
+    cnt[k] += 1;
+    ctx->ev_pool.push_back(e.a);
+    ctx->ev_pool.push_back(e.b);
+  }
+  ctx->prof.clear();
+  int n = (int)kinds.size() < max_kinds ? (int)kinds.size() : max_kinds;
+  for (int k = 0; k < n; ++k) {
+    strncpy(names + 32 * k, kinds[k].c_str(), 31);
+    names[32 * k + 31] = 0;
+    total_ms[k] = tot[k];
+    count[k] = cnt[k];
+  }
+  *n_kinds = n;
+  return REDVE_OK;
+}
+
 int redve_create(redve_ctx** out, int device) {
   if (!out) return REDVE_E_VALUE;
   redve_ctx* c = new redve_ctx();
@@ -182,8 +268,10 @@ int redve_create(redve_ctx** out, int device) {
     *out = c;
     return fail(c, REDVE_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
   }
-  configure_kernels();
+  int ce = configure_kernels();
   *out = c;
+  if (ce != 0)
+    return fail(c, REDVE_E_CUDA, "configuring kernels: %s", cudaGetErrorString((cudaError_t)ce));
   return REDVE_OK;
 }
 
@@ -211,7 +299,7 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       CK(cudaMemcpyAsync(out, x, sizeof(double) * N * B, cudaMemcpyDeviceToDevice, ctx->stream));
       return REDVE_OK;
     case REDVE_DN_MEDIAN3:
-      launch_median3(x, out, B, H, W, ctx->stream);
+      RUN(ctx, "median3", launch_median3(x, out, B, H, W, ctx->stream));
       CKL();
       return REDVE_OK;
     case REDVE_DN_CONV: {
@@ -221,7 +309,7 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       size_t kb = sizeof(double) * dn->ksize * dn->ksize;
       CK(ctx->scratch_taps.ensure(kb));
       CK(cudaMemcpyAsync(ctx->scratch_taps.p, dn->taps, kb, cudaMemcpyHostToDevice, ctx->stream));
-      launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), dn->ksize, 0, 1.0, ctx->stream);
+      RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), dn->ksize, 0, 1.0, ctx->stream));
       CKL();
       // taps buffer is reused by the next call: keep it alive until then
       CK(cudaStreamSynchronize(ctx->stream));
@@ -258,10 +346,10 @@ int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, i
   if (rc) return rc;
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
-    launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 0, 1.0, ctx->stream);
+    RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 0, 1.0, ctx->stream));
   } else {
-    launch_decimate_conv(x, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
-                         ctx->stream);
+    RUN(ctx, "decimate_conv", launch_decimate_conv(x, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
+                         ctx->stream));
   }
   CKL();
   CK(cudaStreamSynchronize(ctx->stream));
@@ -274,10 +362,10 @@ int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B,
   if (rc) return rc;
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
-    launch_conv(z, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 1, 1.0, ctx->stream);
+    RUN(ctx, "conv", launch_conv(z, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 1, 1.0, ctx->stream));
   } else {
-    launch_upsample_corr(z, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
-                         1.0, ctx->stream);
+    RUN(ctx, "upsample_corr", launch_upsample_corr(z, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
+                         1.0, ctx->stream));
   }
   CKL();
   CK(cudaStreamSynchronize(ctx->stream));
@@ -360,7 +448,7 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
                        s));
   }
   PK(p->state.ensure(sizeof(ImgState) * B));
-  launch_init_state(p->state.as<ImgState>(), B, s);
+  RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), B, s));
   int nblk_row = (H + p->lpc_row - 1) / p->lpc_row;
   int nblk_cost = (H + cost_rows(H) - 1) / cost_rows(H);
   size_t part = (size_t)p->npairs * (nblk_row > nblk_cost ? nblk_row : nblk_cost) * 6;
@@ -374,8 +462,8 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   PK(p->vals.ensure(sizeof(double) * 3 * B));
   // H^T y / sigma^2 (objective.py:70)
   PK(p->hty.ensure(sizeof(double) * p->N * B));
-  launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W, p->htaps.as<double>(),
-              op->ksize, 1, 1.0 / (sigma * sigma), s);
+  RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W, p->htaps.as<double>(),
+              op->ksize, 1, 1.0 / (sigma * sigma), s));
   PK(cudaGetLastError());
   if (p->fourier) {
     p->twH = ctx->tw(H);
@@ -385,7 +473,7 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
       return bail(REDVE_E_CUDA);
     }
     PK(p->g.ensure(sizeof(double) * p->N));
-    launch_inv_denom(p->g.as<double>(), H, W, p->htaps.as<double>(), op->ksize, sigma, alpha, s);
+    RUN(ctx, "inv_denom", launch_inv_denom(p->g.as<double>(), H, W, p->htaps.as<double>(), op->ksize, sigma, alpha, s));
     PK(cudaGetLastError());
     PK(p->Z.ensure(sizeof(cd) * p->N * p->npairs));
     PK(p->xb.ensure(sizeof(double) * p->N * B));
@@ -410,7 +498,7 @@ int redve_fp_step(redve_problem* p, const double* x, double* out, const double* 
   redve_ctx* ctx = p->ctx;
   if (p->dn_kind == DN_EXTERNAL && !f_ext)
     return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
-  launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream);
+  RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream));
   DenoiseArgs dn = dn_args(p);
   View xin = plain(x, p->N);
   if (p->dn_kind == DN_EXTERNAL) {
@@ -451,7 +539,7 @@ int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* c
   TraceBufs tr;
   memset(&tr, 0, sizeof(tr));
   CostArgs a = cost_args(p, plain(x, p->N), f_ext, COST_VALUE, ctl, tr);
-  launch_cost(a, p->npairs, ctx->stream);
+  RUN(ctx, "cost", launch_cost(a, p->npairs, ctx->stream));
   CKL();
   std::vector<double> v(3 * p->B);
   CK(cudaMemcpyAsync(v.data(), p->vals.p, sizeof(double) * 3 * p->B, cudaMemcpyDeviceToHost,
@@ -546,7 +634,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
                                          sizeof(int) * ncyc * 4, s));
   ImgState* st = p->state.as<ImgState>();
-  launch_init_state(st, B, s);
+  RUN(ctx, "init_state", launch_init_state(st, B, s));
   CKL();
   // x0 -> ring slot 0
   CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * N * S, x0, sizeof(double) * N,
@@ -567,9 +655,9 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
 
   if (track) {  // note_initial (solvers.py:219-223)
     CostArgs ca = cost_args(p, cur, nullptr, COST_INIT, ctl, tr);
-    launch_cost(ca, p->npairs, s);
+    RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
     CKL();
-    launch_copy_view(bestv, cur, B, N, st, 1, s);
+    RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
     CKL();
   }
 
@@ -582,10 +670,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     if (r) return r;
     if (cadence) {
       CostArgs ca = cost_args(p, cur, nullptr, COST_RECORD, c, tr);
-      launch_cost(ca, p->npairs, s);
+      RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
       CKL();
       if (track) {
-        launch_copy_view(bestv, cur, B, N, st, 1, s);
+        RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
         CKL();
       }
     }
@@ -626,11 +714,11 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         if (k >= budget) break;
       }
       if (n == clen) {
-        launch_gram(va, s);
+        RUN(ctx, "gram", launch_gram(va, s));
         CKL();
-        launch_mgs(va, s);
+        RUN(ctx, "mgs", launch_mgs(va, s));
         CKL();
-        launch_combine(va, s);
+        RUN(ctx, "combine", launch_combine(va, s));
         CKL();
       }
       if (k >= budget) break;
@@ -647,10 +735,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   }
   if (track) {  // finalize (solvers.py:255-262)
     CostArgs ca = cost_args(p, cur, nullptr, COST_FINAL, ctl, tr);
-    launch_cost(ca, p->npairs, s);
+    RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
     CKL();
   }
-  launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s);
+  RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s));
   CKL();
 
   // trace back to the host
@@ -698,9 +786,9 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
                      cudaMemcpyDeviceToDevice, s));
   CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
   ImgState* st = ctx->ve_state.as<ImgState>();
-  launch_init_state(st, B, s);
+  RUN(ctx, "init_state", launch_init_state(st, B, s));
   CKL();
-  launch_window_extrapolate_setup(st, B, rows, 0, s);
+  RUN(ctx, "window_extrapolate_setup", launch_window_extrapolate_setup(st, B, rows, 0, s));
   CKL();
   int chunks = (int)((n + 256 * 8 - 1) / (256 * 8));
   if (chunks > 64) chunks = 64;
@@ -730,16 +818,16 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
   va.st = st; va.tr = tr; va.partials = ctx->ve_partials.as<double>();
   va.counters = ctx->ve_counters.as<unsigned>(); va.qscratch = ctx->ve_q.as<double>();
   va.method = method; va.rank_tol = rank_tol; va.chunks = chunks;
-  launch_gram(va, s);
+  RUN(ctx, "gram", launch_gram(va, s));
   CKL();
-  launch_mgs(va, s);
+  RUN(ctx, "mgs", launch_mgs(va, s));
   CKL();
   std::vector<ImgState> pre(B);
   CK(cudaMemcpyAsync(pre.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
-  launch_combine(va, s);
+  RUN(ctx, "combine", launch_combine(va, s));
   CKL();
   View curv{ctx->ve_ring.as<double>(), n * rows, n, rows, 1};
-  launch_gather(out, curv, nullptr, B, n, st, s);
+  RUN(ctx, "gather", launch_gather(out, curv, nullptr, B, n, st, s));
   CKL();
   std::vector<ImgState> post(B);
   CK(cudaMemcpyAsync(post.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));

@@ -29,12 +29,25 @@ __global__ void k_cost(CostArgs a);
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // --------------------------------------------------------------- setup
-void configure_kernels() {
-  const int big = 227 * 1024;
-  cudaFuncSetAttribute(k_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  cudaFuncSetAttribute(k_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+template <class K>
+static cudaError_t allow_big_smem(K kernel, int optin) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes);
+}
+int configure_kernels() {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaError_t e = cudaSuccess, r;
+  if ((r = allow_big_smem(k_row_fwd, optin)) != cudaSuccess) e = r;
+  if ((r = allow_big_smem(k_col, optin)) != cudaSuccess) e = r;
+  if ((r = allow_big_smem(k_row_inv, optin)) != cudaSuccess) e = r;
+  if ((r = allow_big_smem(k_cost, optin)) != cudaSuccess) e = r;
+  cudaGetLastError();
+  return (int)e;
 }
 
 __global__ void k_twiddles(cd* tw, int L) {

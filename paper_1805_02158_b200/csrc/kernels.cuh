@@ -83,7 +83,7 @@ struct VeArgs {
 };
 
 // launchers (kernels.cu)
-void configure_kernels();
+int configure_kernels();  // returns a cudaError_t
 void launch_twiddles(cd* tw, int L, cudaStream_t s);
 void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, double sigma,
                       double alpha, cudaStream_t s);
