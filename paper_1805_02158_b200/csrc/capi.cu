@@ -142,6 +142,8 @@ struct redve_problem {
   double sigma, alpha;
   bool fourier;
   int lpc_row, lpc_col;
+  int separable = 0;
+  DevBuf hsep;  // [u | v] when the PSF is rank one
   DevBuf htaps, dntaps, y, ref, hty, xb, g, Z, state, partials, cnt_inv, cnt_cost, cnt_ve,
       fbuf, ring, best, q, trace, vals;
   bool has_ref = false;
@@ -434,6 +436,30 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   const size_t kb = sizeof(double) * op->ksize * op->ksize;
   PK(p->htaps.ensure(kb));
   PK(cudaMemcpyAsync(p->htaps.p, op->taps, kb, cudaMemcpyHostToDevice, s));
+  {  // rank-one PSF? taps[a][b] == u[a] v[b] (uniform and Gaussian kernels are)
+    const int k = op->ksize;
+    int a0 = 0, b0 = 0;
+    double best = -1.0;
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b)
+        if (std::fabs(op->taps[a * k + b]) > best) {
+          best = std::fabs(op->taps[a * k + b]);
+          a0 = a;
+          b0 = b;
+        }
+    std::vector<double> uv(2 * k);
+    for (int a = 0; a < k; ++a) uv[a] = op->taps[a * k + b0];
+    for (int b = 0; b < k; ++b) uv[k + b] = op->taps[a0 * k + b] / op->taps[a0 * k + b0];
+    bool sep = best > 0;
+    for (int a = 0; a < k && sep; ++a)
+      for (int b = 0; b < k && sep; ++b)
+        sep = std::fabs(uv[a] * uv[k + b] - op->taps[a * k + b]) <= 1e-15 * best;
+    if (sep && k > 1) {
+      p->separable = 1;
+      PK(p->hsep.ensure(sizeof(double) * 2 * k));
+      PK(cudaMemcpy(p->hsep.p, uv.data(), sizeof(double) * 2 * k, cudaMemcpyHostToDevice));
+    }
+  }
   size_t db = dn->kind == REDVE_DN_CONV ? sizeof(double) * dn->ksize * dn->ksize : 8;
   PK(p->dntaps.ensure(db));
   if (dn->kind == REDVE_DN_CONV)
@@ -523,6 +549,9 @@ static CostArgs cost_args(redve_problem* p, View x, const double* f_ext, int mod
   a.dn = dn_args(p);
   a.fext = f_ext;
   a.htaps = p->htaps.as<double>(); a.hk = p->op.ksize;
+  a.separable = p->separable;
+  a.hu = p->separable ? p->hsep.as<double>() : nullptr;
+  a.hv = p->separable ? p->hsep.as<double>() + p->op.ksize : nullptr;
   a.sigma = p->sigma; a.alpha = p->alpha;
   a.mode = mode; a.out_vals = p->vals.as<double>();
   a.st = p->state.as<ImgState>(); a.ctl = ctl; a.tr = tr;

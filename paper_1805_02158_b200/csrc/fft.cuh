@@ -250,6 +250,70 @@ __device__ __forceinline__ void line_fft(cd (&v)[16], cd* sm, const cd* tw, int 
   }
 }
 
+// ------------------------------------------------------------------
+// Compile-time specialisation (L a power of two, 16 <= L <= 4096): every
+// radix, stride and register index is a constant, so the 16 values stay in
+// registers without spills.  FIRST_SMEM: the first stage reads its inputs
+// from shared memory (the caller stored them with the same layout) instead of
+// the registers.
+template <int L, int R, int NS, bool FIRST, bool FIRST_SMEM, bool LAST, bool INV, class Lay>
+__device__ __forceinline__ void ct_stage(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+                                         const Lay& lay) {
+  constexpr int T = L / 16, NB = 16 / R, LR = L / R;
+  cd a[16];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + T * b;
+    const int k = j & (NS - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      cd x;
+      if (FIRST && !FIRST_SMEM) x = v[b * R + r];
+      else x = ld_cd(sm + lay.at(line, j + r * LR));
+      if (!FIRST && r > 0) {
+        const int e = r * k * (L / (NS * R));
+        const cd w = tw[e];
+        x = INV ? cmul(x, w) : cmulc(x, w);
+      }
+      a[b * R + r] = x;
+    }
+    Dft<R, INV>::run(a + b * R);
+  }
+  if (!FIRST || FIRST_SMEM) __syncthreads();  // all reads done before in-place writes
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + T * b;
+    const int k = j & (NS - 1);
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (LAST) v[b + r * NB] = a[b * R + r];
+      else st_cd(sm + lay.at(line, base + r * NS), a[b * R + r]);
+    }
+  }
+  if (!LAST) __syncthreads();
+}
+
+template <int L, int NS, int REM, bool FIRST, bool FIRST_SMEM, bool INV, class Lay>
+struct CtStages {
+  static __device__ __forceinline__ void run(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+                                             const Lay& lay) {
+    constexpr int R = REM >= 16 ? 16 : REM;
+    constexpr bool LAST = (REM == R);
+    ct_stage<L, R, NS, FIRST, FIRST_SMEM, LAST, INV>(v, sm, tw, t, line, lay);
+    if constexpr (!LAST)
+      CtStages<L, NS * R, REM / R, false, false, INV, Lay>::run(v, sm, tw, t, line, lay);
+  }
+};
+
+// Register contract as line_fft; L must be a power of two >= 16.
+template <int L, bool INV, bool FIRST_SMEM = false, class Lay>
+__device__ __forceinline__ void line_fft_ct(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+                                            const Lay& lay) {
+  static_assert(L >= 16 && (L & (L - 1)) == 0, "compile-time FFT needs a power of two >= 16");
+  CtStages<L, 1, L, true, FIRST_SMEM, INV, Lay>::run(v, sm, tw, t, line, lay);
+}
+
 // Twiddle table W_L^m = exp(+2 pi i m / L), m < L, into shared memory.
 __device__ __forceinline__ void load_twiddles(cd* dst, const cd* src, int L) {
   for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = ldg_cd(src + i);

@@ -1,0 +1,321 @@
+// Fused Fourier fixed-point step for circulant H (objective.py:100-104), fp64.
+//
+//   x+ = x_b + IDFT( alpha g . DFT f(x) ),  g = 1/((|H^|^2/sigma^2 + alpha) H W)
+//   x_b = IDFT( g . DFT(H^T y / sigma^2) )            (precomputed once)
+//
+// The step is linear in its right-hand side, so splitting off x_b is exact
+// algebra.  Two images of the batch ride as one complex image (re = 2p,
+// im = 2p+1): g is real and even, so the complex transform of the pair gives
+// both real results.  Three kernels per step, each streaming HBM once:
+//
+//   k_row_fwd : x tile (+halo) -> denoiser -> row FFTs            -> Z   (2 B N s)
+//   k_col     : Z columns -> FFT -> * alpha g -> inverse FFT       -> Z   (2 B N s)
+//   k_row_inv : Z rows -> inverse FFT -> + x_b -> x+, step-norm record    (4 B N s)
+//
+// Sizes that are powers of two in [16, 1024] use compile-time FFT plans;
+// anything else the runtime plan (direct DFT for non powers of two).
+#include "kernels.cuh"
+
+namespace redve {
+
+extern __shared__ __align__(16) unsigned char f_smem[];
+
+static inline __host__ __device__ size_t al16f(size_t b) { return (b + 15) & ~size_t(15); }
+static inline int cdivf(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+size_t row_fwd_smem(int W, int lpc, int radius, int ksize) {
+  size_t tile = (size_t)(lpc + 2 * radius) * W * sizeof(cd);
+  size_t lines = (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd);
+  return al16f(W * sizeof(cd)) + al16f((size_t)ksize * ksize * sizeof(double)) +
+         (tile > lines ? tile : lines);
+}
+size_t col_smem(int H, int lpc) { return al16f(H * sizeof(cd)) + (size_t)H * lpc * sizeof(cd); }
+size_t row_inv_smem(int W, int lpc) {
+  return al16f(W * sizeof(cd)) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
+         al16f(32 * 6 * sizeof(double));
+}
+
+template <int L, bool INV, class Lay>
+__device__ __forceinline__ void fft_dispatch(cd (&v)[16], cd* sm, const cd* tw, int Lrt, int t,
+                                             int line, const Lay& lay) {
+  if constexpr (L > 0) {
+    line_fft_ct<L, INV>(v, sm, tw, t, line, lay);
+  } else {
+    line_fft<INV>(v, sm, tw, Lrt, t, line, lay);
+  }
+}
+
+// --------------------------------------------------------------- row forward
+template <int LW, int DK>
+__global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const bool a0 = takes_step(a.st[b0], a.phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
+  if (!a0 && !a1) return;
+  const int W = LW > 0 ? LW : a.W;
+  const int H = a.H;
+  const int T = LW > 0 ? LW / 16 : threads_per_line(W);
+  const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
+  const int ks = DK == DN_CONV ? a.dn.ksize : 0;
+  cd* s_tw = reinterpret_cast<cd*>(f_smem);
+  double* s_taps = reinterpret_cast<double*>(f_smem + al16f(W * sizeof(cd)));
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(W * sizeof(cd)) +
+                                     al16f((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
+  load_twiddles(s_tw, a.tw, W);
+  if (DK == DN_CONV)
+    for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
+  const double* x0 = a0 ? a.xin.at(b0, a.st) : nullptr;
+  const double* x1 = a1 ? a.xin.at(b1, a.st) : nullptr;
+  const int r0 = blockIdx.x * a.lpc;
+  const int trows = a.lpc + 2 * R;
+  // tile rows r0-R .. r0+lpc+R-1 (periodic), both images
+  if ((W & 1) == 0) {  // even width: every row (and image) starts 16-byte aligned
+    const int W2 = W >> 1;
+    for (int idx = threadIdx.x; idx < trows * W2; idx += blockDim.x) {
+      const int i = idx / W2, c2 = idx - i * W2;
+      const int gr = wrap(r0 - R + i, H);
+      const long long o = (long long)gr * W + 2 * c2;
+      double2 u0 = x0 ? __ldg(reinterpret_cast<const double2*>(x0 + o)) : make_double2(0.0, 0.0);
+      double2 u1 = x1 ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
+      st_cd(s_work + i * W + 2 * c2, cd{u0.x, u1.x});
+      st_cd(s_work + i * W + 2 * c2 + 1, cd{u0.y, u1.y});
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
+      const int i = idx / W, c = idx - i * W;
+      const long long o = (long long)wrap(r0 - R + i, H) * W + c;
+      st_cd(s_work + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+    }
+  }
+  __syncthreads();
+  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
+  const int row = r0 + line;
+  const bool valid = row < H;
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int c = t + T * m;
+    v[m] = (valid && c < W) ? denoise_at(s_work, W, line + R, c, DK, ks, s_taps) : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  RowLayout lay{RowLayout::stride_for(W)};
+  fft_dispatch<LW, false>(v, s_work, s_tw, W, t, line, lay);
+  if (valid) {
+    cd* zr = a.Z + ((long long)p * H + row) * W;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int c = t + T * m;
+      if (c < W) st_cd(zr + c, v[m]);
+    }
+  }
+}
+
+template <class K>
+static void big_smem_once(K kernel, bool& done) {
+  if (done) return;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)fa.sharedSizeBytes);
+  done = true;
+}
+
+template <int LW, int DK>
+static void row_fwd_t(const RowFwdArgs& a, int npairs, cudaStream_t s) {
+  static bool done = false;
+  big_smem_once(k_row_fwd<LW, DK>, done);
+  const int T = threads_per_line(a.W);
+  dim3 grid(cdivf(a.H, a.lpc), npairs);
+  k_row_fwd<LW, DK><<<grid, a.lpc * T, row_fwd_smem(a.W, a.lpc, a.dn.radius, a.dn.ksize), s>>>(a);
+}
+
+template <int DK>
+static void row_fwd_dk(const RowFwdArgs& a, int npairs, cudaStream_t s) {
+  switch (a.W) {
+    case 64: row_fwd_t<64, DK>(a, npairs, s); break;
+    case 128: row_fwd_t<128, DK>(a, npairs, s); break;
+    case 256: row_fwd_t<256, DK>(a, npairs, s); break;
+    case 512: row_fwd_t<512, DK>(a, npairs, s); break;
+    case 1024: row_fwd_t<1024, DK>(a, npairs, s); break;
+    default: row_fwd_t<0, DK>(a, npairs, s); break;
+  }
+}
+
+void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s) {
+  switch (a.dn.kind) {
+    case DN_CONV: row_fwd_dk<DN_CONV>(a, npairs, s); break;
+    case DN_MEDIAN3: row_fwd_dk<DN_MEDIAN3>(a, npairs, s); break;
+    default: row_fwd_dk<DN_IDENTITY>(a, npairs, s); break;
+  }
+}
+
+// --------------------------------------------------------------- columns
+template <int LH>
+__global__ void __launch_bounds__(256) k_col(ColArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const bool a0 = takes_step(a.st[b0], a.phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
+  if (!a0 && !a1) return;
+  const int H = LH > 0 ? LH : a.H;
+  const int W = a.W;
+  const int T = LH > 0 ? LH / 16 : threads_per_line(H);
+  cd* s_tw = reinterpret_cast<cd*>(f_smem);
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(H * sizeof(cd)));
+  load_twiddles(s_tw, a.tw, H);
+  const int line = threadIdx.x % a.lpc, t = threadIdx.x / a.lpc;
+  const int col = blockIdx.x * a.lpc + line;
+  const bool valid = col < W;
+  cd* zc = a.Z + (long long)p * H * W + (valid ? col : 0);
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int r = t + T * m;
+    v[m] = (valid && r < H) ? ld_cd(zc + (long long)r * W) : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  ColLayout lay{a.lpc};
+  fft_dispatch<LH, false>(v, s_work, s_tw, H, t, line, lay);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int r = t + T * m;
+    if (valid && r < H) v[m] = v[m] * (a.scale * __ldg(a.g + (long long)r * W + col));
+  }
+  fft_dispatch<LH, true>(v, s_work, s_tw, H, t, line, lay);
+  if (valid) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int r = t + T * m;
+      if (r < H) st_cd(zc + (long long)r * W, v[m]);
+    }
+  }
+}
+
+template <int LH>
+static void col_t(const ColArgs& a, int npairs, cudaStream_t s) {
+  static bool done = false;
+  big_smem_once(k_col<LH>, done);
+  const int T = threads_per_line(a.H);
+  dim3 grid(cdivf(a.W, a.lpc), npairs);
+  k_col<LH><<<grid, a.lpc * T, col_smem(a.H, a.lpc), s>>>(a);
+}
+
+void launch_col(const ColArgs& a, int npairs, cudaStream_t s) {
+  switch (a.H) {
+    case 64: col_t<64>(a, npairs, s); break;
+    case 128: col_t<128>(a, npairs, s); break;
+    case 256: col_t<256>(a, npairs, s); break;
+    case 512: col_t<512>(a, npairs, s); break;
+    case 1024: col_t<1024>(a, npairs, s); break;
+    default: col_t<0>(a, npairs, s); break;
+  }
+}
+
+// --------------------------------------------------------------- row inverse
+template <int LW>
+__global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
+  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
+  const bool a0 = takes_step(a.st[b0], phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
+  if (!a0 && !a1) return;
+  const int W = LW > 0 ? LW : a.W;
+  const int H = a.H;
+  const int T = LW > 0 ? LW / 16 : threads_per_line(W);
+  const long long N = (long long)H * W;
+  cd* s_tw = reinterpret_cast<cd*>(f_smem);
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(W * sizeof(cd)));
+  double* s_red = reinterpret_cast<double*>(f_smem + al16f(W * sizeof(cd)) +
+                                            (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
+  load_twiddles(s_tw, a.tw, W);
+  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
+  const int row = blockIdx.x * a.lpc + line;
+  const bool valid = row < H;
+  const cd* zr = a.Z + ((long long)p * H + (valid ? row : 0)) * W;
+  cd v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int c = t + T * m;
+    v[m] = (valid && c < W) ? ld_cd(zr + c) : cd{0.0, 0.0};
+  }
+  __syncthreads();
+  RowLayout lay{RowLayout::stride_for(W)};
+  fft_dispatch<LW, true>(v, s_work, s_tw, W, t, line, lay);
+
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  if (valid) {
+    double* o0 = a0 ? a.out.at(b0, a.st) + (long long)row * W : nullptr;
+    double* o1 = a1 ? a.out.at(b1, a.st) + (long long)row * W : nullptr;
+    const double* p0 = (a0 && a.epilogue) ? a.xprev.at(b0, a.st) + (long long)row * W : nullptr;
+    const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) + (long long)row * W : nullptr;
+    const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N + (long long)row * W : nullptr;
+    const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N + (long long)row * W : nullptr;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int c = t + T * m;
+      if (c >= W) continue;
+      if (o0) {
+        const double val = v[m].x + (bs0 ? __ldg(bs0 + c) : 0.0);
+        o0[c] = val;
+        if (p0) {
+          const double xp = __ldg(p0 + c), d = val - xp;
+          acc[0] = fma(d, d, acc[0]);
+          acc[1] = fma(xp, xp, acc[1]);
+          acc[2] += isfinite(val) ? 0.0 : 1.0;
+        }
+      }
+      if (o1) {
+        const double val = v[m].y + (bs1 ? __ldg(bs1 + c) : 0.0);
+        o1[c] = val;
+        if (p1) {
+          const double xp = __ldg(p1 + c), d = val - xp;
+          acc[3] = fma(d, d, acc[3]);
+          acc[4] = fma(xp, xp, acc[4]);
+          acc[5] += isfinite(val) ? 0.0 : 1.0;
+        }
+      }
+    }
+  }
+  if (!a.epilogue) return;
+  block_sum<6>(acc, s_red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) {
+    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (int blk = 0; blk < nblk; ++blk) {
+      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
+      for (int i = 0; i < 6; ++i) tot[i] += src[i];
+    }
+    if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
+    if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
+  }
+}
+
+template <int LW>
+static void row_inv_t(const RowInvArgs& a, int npairs, cudaStream_t s) {
+  static bool done = false;
+  big_smem_once(k_row_inv<LW>, done);
+  const int T = threads_per_line(a.W);
+  dim3 grid(cdivf(a.H, a.lpc), npairs);
+  k_row_inv<LW><<<grid, a.lpc * T, row_inv_smem(a.W, a.lpc), s>>>(a);
+}
+
+void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s) {
+  switch (a.W) {
+    case 64: row_inv_t<64>(a, npairs, s); break;
+    case 128: row_inv_t<128>(a, npairs, s); break;
+    case 256: row_inv_t<256>(a, npairs, s); break;
+    case 512: row_inv_t<512>(a, npairs, s); break;
+    case 1024: row_inv_t<1024>(a, npairs, s); break;
+    default: row_inv_t<0>(a, npairs, s); break;
+  }
+}
+
+}  // namespace redve

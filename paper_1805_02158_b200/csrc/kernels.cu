@@ -21,16 +21,17 @@ namespace redve {
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 
-__global__ void k_row_fwd(RowFwdArgs a);
-__global__ void k_col(ColArgs a);
-__global__ void k_row_inv(RowInvArgs a);
-__global__ void k_cost(CostArgs a);
 
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // --------------------------------------------------------------- setup
 template <class K>
 static cudaError_t allow_big_smem(K kernel, int optin) {
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
   if (e != cudaSuccess) return e;
@@ -42,10 +43,6 @@ int configure_kernels() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaError_t e = cudaSuccess, r;
-  if ((r = allow_big_smem(k_row_fwd, optin)) != cudaSuccess) e = r;
-  if ((r = allow_big_smem(k_col, optin)) != cudaSuccess) e = r;
-  if ((r = allow_big_smem(k_row_inv, optin)) != cudaSuccess) e = r;
-  if ((r = allow_big_smem(k_cost, optin)) != cudaSuccess) e = r;
   cudaGetLastError();
   return (int)e;
 }
@@ -93,229 +90,7 @@ void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, doubl
   k_inv_denom<<<cdiv((long long)H * W, 128), 128, 0, s>>>(g, H, W, taps, hk, sigma, alpha);
 }
 
-// --------------------------------------------------------------- smem plans
 static inline __host__ __device__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
-
-size_t row_fwd_smem(int W, int lpc, int radius, int ksize) {
-  size_t tile = (size_t)(lpc + 2 * radius) * W * sizeof(cd);
-  size_t lines = (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd);
-  return al16(W * sizeof(cd)) + al16((size_t)ksize * ksize * sizeof(double)) +
-         (tile > lines ? tile : lines);
-}
-size_t col_smem(int H, int lpc) { return al16(H * sizeof(cd)) + (size_t)H * lpc * sizeof(cd); }
-size_t row_inv_smem(int W, int lpc) {
-  return al16(W * sizeof(cd)) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
-         al16(32 * 6 * sizeof(double));
-}
-
-// --------------------------------------------------------------- row forward
-__global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
-  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const bool a0 = takes_step(a.st[b0], a.phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
-  if (!a0 && !a1) return;
-  const int W = a.W, H = a.H, T = threads_per_line(W), R = a.dn.radius;
-  const int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
-  cd* s_tw = reinterpret_cast<cd*>(g_smem);
-  double* s_taps = reinterpret_cast<double*>(g_smem + al16(W * sizeof(cd)));
-  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(W * sizeof(cd)) +
-                                     al16((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
-  load_twiddles(s_tw, a.tw, W);
-  for (int i = threadIdx.x; i < kk; i += blockDim.x) s_taps[i] = a.dn.taps[i];
-  const double* x0 = a0 ? a.xin.at(b0, a.st) : nullptr;
-  const double* x1 = a1 ? a.xin.at(b1, a.st) : nullptr;
-  const int r0 = blockIdx.x * a.lpc;
-  const int trows = a.lpc + 2 * R;
-  for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
-    int i = idx / W, c = idx - i * W;
-    int gr = wrap(r0 - R + i, H);
-    long long o = (long long)gr * W + c;
-    st_cd(s_work + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
-  }
-  __syncthreads();
-  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
-  const int row = r0 + line;
-  const bool valid = row < H;
-  cd v[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    int c = t + T * m;
-    v[m] = (valid && c < W) ? denoise_at(s_work, W, line + R, c, a.dn.kind, a.dn.ksize, s_taps)
-                            : cd{0.0, 0.0};
-  }
-  __syncthreads();
-  RowLayout lay{RowLayout::stride_for(W)};
-  line_fft<false>(v, s_work, s_tw, W, t, line, lay);
-  if (valid) {
-    cd* zr = a.Z + ((long long)p * H + row) * W;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      int c = t + T * m;
-      if (c < W) st_cd(zr + c, v[m]);
-    }
-  }
-}
-void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s) {
-  int T = threads_per_line(a.W);
-  size_t sm = row_fwd_smem(a.W, a.lpc, a.dn.radius, a.dn.ksize);
-  dim3 grid(cdiv(a.H, a.lpc), npairs);
-  k_row_fwd<<<grid, a.lpc * T, sm, s>>>(a);
-}
-
-// --------------------------------------------------------------- columns
-__global__ void __launch_bounds__(256) k_col(ColArgs a) {
-  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const bool a0 = takes_step(a.st[b0], a.phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
-  if (!a0 && !a1) return;
-  const int H = a.H, W = a.W, T = threads_per_line(H);
-  cd* s_tw = reinterpret_cast<cd*>(g_smem);
-  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(H * sizeof(cd)));
-  load_twiddles(s_tw, a.tw, H);
-  const int line = threadIdx.x % a.lpc, t = threadIdx.x / a.lpc;
-  const int col = blockIdx.x * a.lpc + line;
-  const bool valid = col < W;
-  cd* zc = a.Z + (long long)p * H * W + col;
-  cd v[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    int r = t + T * m;
-    v[m] = (valid && r < H) ? ld_cd(zc + (long long)r * W) : cd{0.0, 0.0};
-  }
-  __syncthreads();
-  ColLayout lay{a.lpc};
-  line_fft<false>(v, s_work, s_tw, H, t, line, lay);
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    int r = t + T * m;
-    if (valid && r < H) v[m] = v[m] * (a.scale * __ldg(a.g + (long long)r * W + col));
-  }
-  line_fft<true>(v, s_work, s_tw, H, t, line, lay);
-  if (valid) {
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      int r = t + T * m;
-      if (r < H) st_cd(zc + (long long)r * W, v[m]);
-    }
-  }
-}
-void launch_col(const ColArgs& a, int npairs, cudaStream_t s) {
-  int T = threads_per_line(a.H);
-  dim3 grid(cdiv(a.W, a.lpc), npairs);
-  k_col<<<grid, a.lpc * T, col_smem(a.H, a.lpc), s>>>(a);
-}
-
-// --------------------------------------------------------------- record
-// solvers.py:225-253 (_Recorder.record) minus the cost/psnr part (k_cost).
-__device__ void record_step(ImgState& s, int b, double d2, double x2, double nf, int S,
-                            const StepCtl& ctl, const TraceBufs& tr) {
-  s.stepped = 1;
-  s.k += 1;
-  s.cur = (s.cur + 1) % S;
-  double den = sqrt(x2);
-  if (den == 0.0) den = 1.0;
-  const double sn = sqrt(d2) / den;
-  const long long i = (long long)b * tr.cap + (s.k - 1);
-  if (s.k - 1 < tr.cap) {
-    tr.step_norm[i] = sn;
-    tr.elapsed[i] = (double)(globaltimer_ns() - s.t0) * 1e-9;
-  }
-  if (nf > 0.0) s.err = ERR_NONFINITE_X;
-  s.pending = RUNNING;
-  if (ctl.phase == PH_MAIN) {
-    if (sn <= ctl.tol) s.pending = CONVERGED;
-    else if (s.k >= ctl.budget) s.pending = BUDGET;
-  }
-  if (!ctl.defer_commit) commit_step(s, ctl.phase);
-}
-
-// --------------------------------------------------------------- row inverse
-__global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
-  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
-  const bool a0 = takes_step(a.st[b0], phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
-  if (!a0 && !a1) return;
-  const int W = a.W, H = a.H, T = threads_per_line(W);
-  const long long N = (long long)H * W;
-  cd* s_tw = reinterpret_cast<cd*>(g_smem);
-  cd* s_work = reinterpret_cast<cd*>(g_smem + al16(W * sizeof(cd)));
-  double* s_red = reinterpret_cast<double*>(g_smem + al16(W * sizeof(cd)) +
-                                            (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
-  load_twiddles(s_tw, a.tw, W);
-  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
-  const int row = blockIdx.x * a.lpc + line;
-  const bool valid = row < H;
-  const cd* zr = a.Z + ((long long)p * H + (valid ? row : 0)) * W;
-  cd v[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    int c = t + T * m;
-    v[m] = (valid && c < W) ? ld_cd(zr + c) : cd{0.0, 0.0};
-  }
-  __syncthreads();
-  RowLayout lay{RowLayout::stride_for(W)};
-  line_fft<true>(v, s_work, s_tw, W, t, line, lay);
-
-  double acc[6] = {0, 0, 0, 0, 0, 0};
-  if (valid) {
-    double* o0 = a0 ? a.out.at(b0, a.st) : nullptr;
-    double* o1 = a1 ? a.out.at(b1, a.st) : nullptr;
-    const double* p0 = (a0 && a.epilogue) ? a.xprev.at(b0, a.st) : nullptr;
-    const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) : nullptr;
-    const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N : nullptr;
-    const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N : nullptr;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      int c = t + T * m;
-      if (c >= W) continue;
-      long long o = (long long)row * W + c;
-      if (o0) {
-        double val = v[m].x + (bs0 ? __ldg(bs0 + o) : 0.0);
-        o0[o] = val;
-        if (p0) {
-          double xp = __ldg(p0 + o), d = val - xp;
-          acc[0] = fma(d, d, acc[0]);
-          acc[1] = fma(xp, xp, acc[1]);
-          acc[2] += isfinite(val) ? 0.0 : 1.0;
-        }
-      }
-      if (o1) {
-        double val = v[m].y + (bs1 ? __ldg(bs1 + o) : 0.0);
-        o1[o] = val;
-        if (p1) {
-          double xp = __ldg(p1 + o), d = val - xp;
-          acc[3] = fma(d, d, acc[3]);
-          acc[4] = fma(xp, xp, acc[4]);
-          acc[5] += isfinite(val) ? 0.0 : 1.0;
-        }
-      }
-    }
-  }
-  if (!a.epilogue) return;
-  block_sum<6>(acc, s_red);
-  const int nblk = gridDim.x;
-  if (threadIdx.x == 0) {
-    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
-  }
-  __shared__ int s_last;
-  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
-      for (int i = 0; i < 6; ++i) tot[i] += src[i];
-    }
-    if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
-    if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
-  }
-}
-void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s) {
-  int T = threads_per_line(a.W);
-  dim3 grid(cdiv(a.H, a.lpc), npairs);
-  k_row_inv<<<grid, a.lpc * T, row_inv_smem(a.W, a.lpc), s>>>(a);
-}
 
 // --------------------------------------------------------------- cost
 // E(x) = ||Hx - y||^2/(2 sigma^2) + alpha/2 x.(x - f(x))   (objective.py:78-88)
@@ -367,6 +142,7 @@ __device__ __forceinline__ bool cost_wants(const ImgState& s, const CostArgs& a)
   return s.err == ERR_NONE;  // final
 }
 
+template <int DK>
 __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
   const bool has1 = b1 < a.B;
@@ -384,27 +160,63 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   const int W = a.W, H = a.H;
   const long long N = (long long)H * W;
   const int rH = a.hk / 2;
-  const int R = max(rH, a.dn.kind == DN_EXTERNAL ? 0 : a.dn.radius);
-  const int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  const int Rd = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
+  const int R = max(rH, Rd);
+  const int kk = DK == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
   double* s_h = reinterpret_cast<double*>(g_smem);
-  double* s_taps = s_h + a.hk * a.hk;
+  double* s_taps = s_h + a.hk * a.hk + 2 * a.hk;
   double* s_red = s_taps + kk;
-  cd* tile = reinterpret_cast<cd*>(g_smem + al16((a.hk * a.hk + kk + 32 * 3 * 2) * sizeof(double)));
+  cd* tile = reinterpret_cast<cd*>(
+      g_smem + al16((a.hk * a.hk + 2 * a.hk + kk + 32 * 3 * 2) * sizeof(double)));
+  cd* vbuf = tile + (size_t)(a.rows + 2 * R) * W;
+  double* s_u = s_h + a.hk * a.hk;
+  double* s_v = s_u + a.hk;
   for (int i = threadIdx.x; i < a.hk * a.hk; i += blockDim.x) s_h[i] = a.htaps[i];
+  if (a.separable)
+    for (int i = threadIdx.x; i < a.hk; i += blockDim.x) {
+      s_u[i] = a.hu[i];
+      s_v[i] = a.hv[i];
+    }
   for (int i = threadIdx.x; i < kk; i += blockDim.x) s_taps[i] = a.dn.taps[i];
   const double* x0 = w0 ? a.x.at(b0, a.st) : nullptr;
   const double* x1 = w1 ? a.x.at(b1, a.st) : nullptr;
   const int r0 = blockIdx.x * a.rows;
   const int trows = a.rows + 2 * R;
-  for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
-    int i = idx / W, c = idx - i * W;
-    int gr = wrap(r0 - R + i, H);
-    long long o = (long long)gr * W + c;
-    st_cd(tile + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+  if ((W & 1) == 0) {
+    const int W2 = W >> 1;
+    for (int idx = threadIdx.x; idx < trows * W2; idx += blockDim.x) {
+      const int i = idx / W2, c2 = idx - i * W2;
+      const long long o = (long long)wrap(r0 - R + i, H) * W + 2 * c2;
+      double2 u0 = x0 ? __ldg(reinterpret_cast<const double2*>(x0 + o)) : make_double2(0.0, 0.0);
+      double2 u1 = x1 ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
+      st_cd(tile + i * W + 2 * c2, cd{u0.x, u1.x});
+      st_cd(tile + i * W + 2 * c2 + 1, cd{u0.y, u1.y});
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
+      const int i = idx / W, c = idx - i * W;
+      const long long o = (long long)wrap(r0 - R + i, H) * W + c;
+      st_cd(tile + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+    }
   }
   __syncthreads();
-  double acc[6] = {0, 0, 0, 0, 0, 0};  // fid0, reg0, ssd0, fid1, reg1, ssd1
   const int s = a.factor;
+  if (a.separable) {  // vertical pass of the blur on the measurement-grid rows
+    for (int idx = threadIdx.x; idx < a.rows * W; idx += blockDim.x) {
+      const int li = idx / W, c = idx - li * W;
+      const int row = r0 + li;
+      if (row >= H || (row % s) != 0) continue;
+      cd acc = cd{0.0, 0.0};
+      for (int ta = 0; ta < a.hk; ++ta) {
+        const cd xx = ld_cd(tile + (li + R - (ta - rH)) * W + c);
+        acc.x = fma(s_u[ta], xx.x, acc.x);
+        acc.y = fma(s_u[ta], xx.y, acc.y);
+      }
+      st_cd(vbuf + idx, acc);
+    }
+    __syncthreads();
+  }
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // fid0, reg0, ssd0, fid1, reg1, ssd1
   for (int idx = threadIdx.x; idx < a.rows * W; idx += blockDim.x) {
     const int li = idx / W, c = idx - li * W;
     const int row = r0 + li;
@@ -412,11 +224,11 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
     const long long o = (long long)row * W + c;
     const cd xv = ld_cd(tile + (li + R) * W + c);
     cd fv;
-    if (a.dn.kind == DN_EXTERNAL) {
+    if (DK == DN_EXTERNAL) {
       fv = cd{x0 ? __ldg(a.fext + (long long)b0 * N + o) : 0.0,
               x1 ? __ldg(a.fext + (long long)b1 * N + o) : 0.0};
     } else {
-      fv = denoise_at(tile, W, li + R, c, a.dn.kind, a.dn.ksize, s_taps);
+      fv = denoise_at(tile, W, li + R, c, DK, a.dn.ksize, s_taps);
     }
     acc[1] = fma(xv.x, xv.x - fv.x, acc[1]);
     acc[4] = fma(xv.y, xv.y - fv.y, acc[4]);
@@ -433,13 +245,22 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
     if ((row % s) == 0 && (c % s) == 0) {
       // (H x)(row, c) = sum taps[a][b] x[row-(a-r), c-(b-r)], then - y
       cd hx = cd{0.0, 0.0};
-      for (int ta = 0; ta < a.hk; ++ta) {
-        const cd* trow = tile + (li + R - (ta - rH)) * W;
+      if (a.separable) {
+        const cd* vr = vbuf + li * W;
         for (int tb = 0; tb < a.hk; ++tb) {
-          const double w = s_h[ta * a.hk + tb];
-          cd xx = ld_cd(trow + wrap(c - (tb - rH), W));
-          hx.x = fma(w, xx.x, hx.x);
-          hx.y = fma(w, xx.y, hx.y);
+          const cd xx = ld_cd(vr + wrap(c - (tb - rH), W));
+          hx.x = fma(s_v[tb], xx.x, hx.x);
+          hx.y = fma(s_v[tb], xx.y, hx.y);
+        }
+      } else {
+        for (int ta = 0; ta < a.hk; ++ta) {
+          const cd* trow = tile + (li + R - (ta - rH)) * W;
+          for (int tb = 0; tb < a.hk; ++tb) {
+            const double w = s_h[ta * a.hk + tb];
+            const cd xx = ld_cd(trow + wrap(c - (tb - rH), W));
+            hx.x = fma(w, xx.x, hx.x);
+            hx.y = fma(w, xx.y, hx.y);
+          }
         }
       }
       const long long oy = (long long)(row / s) * a.Wy + (c / s);
@@ -482,13 +303,29 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   }
 }
 int cost_rows(int H) { return H < 8 ? H : 8; }
-void launch_cost(const CostArgs& a, int npairs, cudaStream_t s) {
-  int R = max(a.hk / 2, a.dn.kind == DN_EXTERNAL ? 0 : a.dn.radius);
-  int kk = a.dn.kind == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
-  size_t sm = al16((a.hk * a.hk + kk + 32 * 3 * 2) * sizeof(double)) +
-              (size_t)(a.rows + 2 * R) * a.W * sizeof(cd);
+template <int DK>
+static void cost_t(const CostArgs& a, int npairs, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    allow_big_smem(k_cost<DK>, -1);
+    done = true;
+  }
+  const int Rd = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
+  const int R = max(a.hk / 2, Rd);
+  const int kk = DK == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  size_t sm = al16((a.hk * a.hk + 2 * a.hk + kk + 32 * 3 * 2) * sizeof(double)) +
+              (size_t)(a.rows + 2 * R) * a.W * sizeof(cd) +
+              (a.separable ? (size_t)a.rows * a.W * sizeof(cd) : 0);
   dim3 grid(cdiv(a.H, a.rows), npairs);
-  k_cost<<<grid, 256, sm, s>>>(a);
+  k_cost<DK><<<grid, 256, sm, s>>>(a);
+}
+void launch_cost(const CostArgs& a, int npairs, cudaStream_t s) {
+  switch (a.dn.kind) {
+    case DN_CONV: cost_t<DN_CONV>(a, npairs, s); break;
+    case DN_MEDIAN3: cost_t<DN_MEDIAN3>(a, npairs, s); break;
+    case DN_EXTERNAL: cost_t<DN_EXTERNAL>(a, npairs, s); break;
+    default: cost_t<DN_IDENTITY>(a, npairs, s); break;
+  }
 }
 
 // --------------------------------------------------------------- copies

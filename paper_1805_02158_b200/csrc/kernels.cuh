@@ -56,6 +56,9 @@ struct CostArgs {
   const double* fext;  // external f [B][N] (DN_EXTERNAL)
   const double* htaps;
   int hk;
+  int separable;      // htaps == outer(hu, hv): two 1-D passes
+  const double* hu;
+  const double* hv;
   double sigma, alpha;
   int mode;
   double* out_vals;  // COST_VALUE: [B][3] = ||Hx-y||^2, x.(x-f), ||x-ref||^2

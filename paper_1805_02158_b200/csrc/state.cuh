@@ -99,4 +99,29 @@ __device__ __forceinline__ void commit_step(ImgState& s, int phase) {
   s.pending = RUNNING;
 }
 
+// --------------------------------------------------------------- record
+// solvers.py:225-253 (_Recorder.record) minus the cost/psnr part (k_cost).
+__device__ inline void record_step(ImgState& s, int b, double d2, double x2, double nf, int S,
+                            const StepCtl& ctl, const TraceBufs& tr) {
+  s.stepped = 1;
+  s.k += 1;
+  s.cur = (s.cur + 1) % S;
+  double den = sqrt(x2);
+  if (den == 0.0) den = 1.0;
+  const double sn = sqrt(d2) / den;
+  const long long i = (long long)b * tr.cap + (s.k - 1);
+  if (s.k - 1 < tr.cap) {
+    tr.step_norm[i] = sn;
+    tr.elapsed[i] = (double)(globaltimer_ns() - s.t0) * 1e-9;
+  }
+  if (nf > 0.0) s.err = ERR_NONFINITE_X;
+  s.pending = RUNNING;
+  if (ctl.phase == PH_MAIN) {
+    if (sn <= ctl.tol) s.pending = CONVERGED;
+    else if (s.k >= ctl.budget) s.pending = BUDGET;
+  }
+  if (!ctl.defer_commit) commit_step(s, ctl.phase);
+}
+
+
 }  // namespace redve
