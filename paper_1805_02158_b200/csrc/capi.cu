@@ -50,11 +50,12 @@ struct redve_ctx {
   int device = 0;
   cudaStream_t stream = 0;
   std::string err;
-  std::map<int, DevBuf*> twiddles;
+  std::map<int, DevBuf*> twiddles, stage_twiddles;
   DevBuf scratch_taps, scratch_a, scratch_b, ve_ring, ve_state, ve_partials, ve_counters,
       ve_q, ve_trace;
   ~redve_ctx() {
     for (auto& kv : twiddles) delete kv.second;
+    for (auto& kv : stage_twiddles) delete kv.second;
     for (auto& e : prof) {
       cudaEventDestroy(e.a);
       cudaEventDestroy(e.b);
@@ -70,6 +71,20 @@ struct redve_ctx {
       cudaEventCreate(&e);
     }
     return e;
+  }
+  const cd* tws(int L) {  // stage-major table for compile-time plans
+    if (!(L == 64 || L == 128 || L == 256 || L == 512 || L == 1024)) return nullptr;
+    auto it = stage_twiddles.find(L);
+    if (it != stage_twiddles.end()) return it->second->as<cd>();
+    DevBuf* b = new DevBuf();
+    if (b->ensure(sizeof(cd) * tw_stage_size(L)) != cudaSuccess) {
+      delete b;
+      return nullptr;
+    }
+    launch_stage_twiddles(b->as<cd>(), L, stream);
+    g_launches.fetch_add(1);
+    stage_twiddles[L] = b;
+    return b->as<cd>();
   }
   const cd* tw(int L) {
     auto it = twiddles.find(L);
@@ -149,6 +164,8 @@ struct redve_problem {
   bool has_ref = false;
   const cd* twH = nullptr;
   const cd* twW = nullptr;
+  const cd* twsH = nullptr;
+  const cd* twsW = nullptr;
   int ring_S = 0;
 };
 
@@ -169,7 +186,7 @@ static int lines_per_cta(int L) {
 
 static int col_lines_per_cta(int H, int W) {
   int T = threads_per_line(H);
-  int lpc = 256 / T;
+  int lpc = 128 / T;
   if (lpc > 16) lpc = 16;
   if (lpc < 1) lpc = 1;
   return lpc;
@@ -189,17 +206,17 @@ static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double s
                             const double* base, int epilogue, View xprev, StepCtl ctl,
                             TraceBufs tr, int S, int phase) {
   redve_ctx* ctx = p->ctx;
-  RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, p->Z.as<cd>(), p->twW,
+  RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, p->Z.as<cd>(), p->twW, p->twsW,
                 p->state.as<ImgState>(), phase};
   RUN(ctx, "row_fwd", launch_row_fwd(rf, p->npairs, ctx->stream));
   CKL();
-  ColArgs ca{p->B, p->H, p->W, p->lpc_col, p->Z.as<cd>(), p->twH, p->g.as<double>(), scale,
-             p->state.as<ImgState>(), phase};
+  ColArgs ca{p->B, p->H, p->W, p->lpc_col, p->Z.as<cd>(), p->twH, p->twsH, p->g.as<double>(),
+             scale, p->state.as<ImgState>(), phase};
   RUN(ctx, "col", launch_col(ca, p->npairs, ctx->stream));
   CKL();
   RowInvArgs ri;
   ri.B = p->B; ri.H = p->H; ri.W = p->W; ri.lpc = p->lpc_row;
-  ri.Z = p->Z.as<cd>(); ri.tw = p->twW; ri.out = out; ri.base = base; ri.xprev = xprev;
+  ri.Z = p->Z.as<cd>(); ri.tw = p->twW; ri.tws = p->twsW; ri.out = out; ri.base = base; ri.xprev = xprev;
   ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
   ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
   RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
@@ -494,6 +511,8 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   if (p->fourier) {
     p->twH = ctx->tw(H);
     p->twW = ctx->tw(W);
+    p->twsH = ctx->tws(H);
+    p->twsW = ctx->tws(W);
     if (!p->twH || !p->twW) {
       fail(ctx, REDVE_E_CUDA, "twiddle allocation failed");
       return bail(REDVE_E_CUDA);

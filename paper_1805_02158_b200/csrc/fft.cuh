@@ -256,10 +256,36 @@ __device__ __forceinline__ void line_fft(cd (&v)[16], cd* sm, const cd* tw, int 
 // registers without spills.  FIRST_SMEM: the first stage reads its inputs
 // from shared memory (the caller stored them with the same layout) instead of
 // the registers.
+//
+// Twiddles come from a stage-major table: stage (NS, R) owns the block
+// tws[off + r*NS + k] = W_{NS R}^{r k}, so the lanes of a warp (consecutive
+// k) read consecutive entries -- no shared-memory bank conflicts.
+constexpr int tw_stage_size(int L) {
+  int ns = 16, rem = L / 16, sz = 0;
+  while (rem > 1) {
+    int R = rem >= 16 ? 16 : rem;
+    sz += R * ns;
+    ns *= R;
+    rem /= R;
+  }
+  return sz;
+}
+constexpr int tw_stage_offset(int L, int NS) {
+  int ns = 16, rem = L / 16, off = 0;
+  while (ns < NS) {
+    int R = rem >= 16 ? 16 : rem;
+    off += R * ns;
+    ns *= R;
+    rem /= R;
+  }
+  return off;
+}
+
 template <int L, int R, int NS, bool FIRST, bool FIRST_SMEM, bool LAST, bool INV, class Lay>
-__device__ __forceinline__ void ct_stage(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+__device__ __forceinline__ void ct_stage(cd (&v)[16], cd* sm, const cd* tws, int t, int line,
                                          const Lay& lay) {
   constexpr int T = L / 16, NB = 16 / R, LR = L / R;
+  constexpr int OFF = FIRST ? 0 : tw_stage_offset(L, NS);
   cd a[16];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
@@ -271,8 +297,7 @@ __device__ __forceinline__ void ct_stage(cd (&v)[16], cd* sm, const cd* tw, int 
       if (FIRST && !FIRST_SMEM) x = v[b * R + r];
       else x = ld_cd(sm + lay.at(line, j + r * LR));
       if (!FIRST && r > 0) {
-        const int e = r * k * (L / (NS * R));
-        const cd w = tw[e];
+        const cd w = tws[OFF + r * NS + k];
         x = INV ? cmul(x, w) : cmulc(x, w);
       }
       a[b * R + r] = x;
@@ -296,22 +321,23 @@ __device__ __forceinline__ void ct_stage(cd (&v)[16], cd* sm, const cd* tw, int 
 
 template <int L, int NS, int REM, bool FIRST, bool FIRST_SMEM, bool INV, class Lay>
 struct CtStages {
-  static __device__ __forceinline__ void run(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+  static __device__ __forceinline__ void run(cd (&v)[16], cd* sm, const cd* tws, int t, int line,
                                              const Lay& lay) {
     constexpr int R = REM >= 16 ? 16 : REM;
     constexpr bool LAST = (REM == R);
-    ct_stage<L, R, NS, FIRST, FIRST_SMEM, LAST, INV>(v, sm, tw, t, line, lay);
+    ct_stage<L, R, NS, FIRST, FIRST_SMEM, LAST, INV>(v, sm, tws, t, line, lay);
     if constexpr (!LAST)
-      CtStages<L, NS * R, REM / R, false, false, INV, Lay>::run(v, sm, tw, t, line, lay);
+      CtStages<L, NS * R, REM / R, false, false, INV, Lay>::run(v, sm, tws, t, line, lay);
   }
 };
 
-// Register contract as line_fft; L must be a power of two >= 16.
+// Register contract as line_fft; L must be a power of two >= 16; tws is the
+// stage-major table of L (tw_stage_size(L) entries).
 template <int L, bool INV, bool FIRST_SMEM = false, class Lay>
-__device__ __forceinline__ void line_fft_ct(cd (&v)[16], cd* sm, const cd* tw, int t, int line,
+__device__ __forceinline__ void line_fft_ct(cd (&v)[16], cd* sm, const cd* tws, int t, int line,
                                             const Lay& lay) {
   static_assert(L >= 16 && (L & (L - 1)) == 0, "compile-time FFT needs a power of two >= 16");
-  CtStages<L, 1, L, true, FIRST_SMEM, INV, Lay>::run(v, sm, tw, t, line, lay);
+  CtStages<L, 1, L, true, FIRST_SMEM, INV, Lay>::run(v, sm, tws, t, line, lay);
 }
 
 // Twiddle table W_L^m = exp(+2 pi i m / L), m < L, into shared memory.

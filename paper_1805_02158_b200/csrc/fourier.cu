@@ -23,16 +23,42 @@ extern __shared__ __align__(16) unsigned char f_smem[];
 static inline __host__ __device__ size_t al16f(size_t b) { return (b + 15) & ~size_t(15); }
 static inline int cdivf(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+static bool ct_size(int L) { return L == 64 || L == 128 || L == 256 || L == 512 || L == 1024; }
+static size_t tw_bytes(int L) { return al16f((ct_size(L) ? tw_stage_size(L) : L) * sizeof(cd)); }
+
 size_t row_fwd_smem(int W, int lpc, int radius, int ksize) {
-  size_t tile = (size_t)(lpc + 2 * radius) * W * sizeof(cd);
+  size_t tile = (size_t)(lpc + 2 * radius) * RowLayout::stride_for(W) * sizeof(cd);
   size_t lines = (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd);
-  return al16f(W * sizeof(cd)) + al16f((size_t)ksize * ksize * sizeof(double)) +
+  return tw_bytes(W) + al16f((size_t)ksize * ksize * sizeof(double)) +
          (tile > lines ? tile : lines);
 }
-size_t col_smem(int H, int lpc) { return al16f(H * sizeof(cd)) + (size_t)H * lpc * sizeof(cd); }
+size_t col_smem(int H, int lpc) { return tw_bytes(H) + (size_t)H * lpc * sizeof(cd); }
 size_t row_inv_smem(int W, int lpc) {
-  return al16f(W * sizeof(cd)) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
+  return tw_bytes(W) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
          al16f(32 * 6 * sizeof(double));
+}
+
+__global__ void k_stage_twiddles(cd* tws, int L) {
+  // stage (NS, R): tws[off + r*NS + k] = exp(2 pi i r k / (NS R))
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  int ns = 16, rem = L / 16, off = 0;
+  while (rem > 1) {
+    const int R = rem >= 16 ? 16 : rem;
+    if (idx >= off && idx < off + R * ns) {
+      const int e = idx - off, r = e / ns, k = e - r * ns;
+      double s, c;
+      sincospi(2.0 * (double)(r * k) / (double)(ns * R), &s, &c);
+      tws[idx] = cd{c, s};
+      return;
+    }
+    off += R * ns;
+    ns *= R;
+    rem /= R;
+  }
+}
+void launch_stage_twiddles(cd* tws, int L, cudaStream_t s) {
+  const int n = tw_stage_size(L);
+  k_stage_twiddles<<<cdivf(n, 256), 256, 0, s>>>(tws, L);
 }
 
 template <int L, bool INV, class Lay>
@@ -46,6 +72,46 @@ __device__ __forceinline__ void fft_dispatch(cd (&v)[16], cd* sm, const cd* tw, 
 }
 
 // --------------------------------------------------------------- row forward
+// Padded tile: element (i, c) at i*stride + c + c/16 -- conflict-free for the
+// contiguous 16-column spans each thread reads.
+struct TileLayout {
+  int stride;
+  __device__ __forceinline__ int at(int i, int c) const { return i * stride + c + (c >> 4); }
+};
+
+template <int LW>
+__device__ __forceinline__ int colwrap(int c, int W) {
+  if constexpr (LW > 0) return c < 0 ? c + W : (c >= W ? c - W : c);  // |c - [0,W)| <= radius
+  else return wrap(c, W);
+}
+
+struct Sorted3 {
+  cd lo, mid, hi;
+};
+__device__ __forceinline__ void sort2c(cd& a, cd& b) {
+  sort2(a.x, b.x);
+  sort2(a.y, b.y);
+}
+__device__ __forceinline__ Sorted3 sorted_col(cd a, cd b, cd c) {
+  sort2c(a, b);
+  sort2c(b, c);
+  sort2c(a, b);
+  return Sorted3{a, b, c};
+}
+__device__ __forceinline__ double med3d(double a, double b, double c) {
+  return fmax(fmin(a, b), fmin(fmax(a, b), c));
+}
+// median of the 3x3 block whose columns are A, B, C (each sorted): exact
+// selection  med3( max(lows), med3(mids), min(highs) ).
+__device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, const Sorted3& C) {
+  cd r;
+  r.x = med3d(fmax(fmax(A.lo.x, B.lo.x), C.lo.x), med3d(A.mid.x, B.mid.x, C.mid.x),
+              fmin(fmin(A.hi.x, B.hi.x), C.hi.x));
+  r.y = med3d(fmax(fmax(A.lo.y, B.lo.y), C.lo.y), med3d(A.mid.y, B.mid.y, C.mid.y),
+              fmin(fmin(A.hi.y, B.hi.y), C.hi.y));
+  return r;
+}
+
 template <int LW, int DK>
 __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
@@ -57,49 +123,95 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int T = LW > 0 ? LW / 16 : threads_per_line(W);
   const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
   const int ks = DK == DN_CONV ? a.dn.ksize : 0;
+  const int ntw = LW > 0 ? tw_stage_size(LW) : W;
   cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  double* s_taps = reinterpret_cast<double*>(f_smem + al16f(W * sizeof(cd)));
-  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(W * sizeof(cd)) +
+  double* s_taps = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)));
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)) +
                                      al16f((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
-  load_twiddles(s_tw, a.tw, W);
+  load_twiddles(s_tw, LW > 0 ? a.tws : a.tw, ntw);
   if (DK == DN_CONV)
     for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
   const double* x0 = a0 ? a.xin.at(b0, a.st) : nullptr;
   const double* x1 = a1 ? a.xin.at(b1, a.st) : nullptr;
   const int r0 = blockIdx.x * a.lpc;
   const int trows = a.lpc + 2 * R;
+  const TileLayout tl{RowLayout::stride_for(W)};
   // tile rows r0-R .. r0+lpc+R-1 (periodic), both images
   if ((W & 1) == 0) {  // even width: every row (and image) starts 16-byte aligned
     const int W2 = W >> 1;
     for (int idx = threadIdx.x; idx < trows * W2; idx += blockDim.x) {
       const int i = idx / W2, c2 = idx - i * W2;
-      const int gr = wrap(r0 - R + i, H);
-      const long long o = (long long)gr * W + 2 * c2;
+      const long long o = (long long)wrap(r0 - R + i, H) * W + 2 * c2;
       double2 u0 = x0 ? __ldg(reinterpret_cast<const double2*>(x0 + o)) : make_double2(0.0, 0.0);
       double2 u1 = x1 ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
-      st_cd(s_work + i * W + 2 * c2, cd{u0.x, u1.x});
-      st_cd(s_work + i * W + 2 * c2 + 1, cd{u0.y, u1.y});
+      st_cd(s_work + tl.at(i, 2 * c2), cd{u0.x, u1.x});
+      st_cd(s_work + tl.at(i, 2 * c2 + 1), cd{u0.y, u1.y});
     }
   } else {
     for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
       const int i = idx / W, c = idx - i * W;
       const long long o = (long long)wrap(r0 - R + i, H) * W + c;
-      st_cd(s_work + idx, cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
+      st_cd(s_work + tl.at(i, c), cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
     }
   }
   __syncthreads();
   const int line = threadIdx.x / T, t = threadIdx.x - line * T;
   const int row = r0 + line;
   const bool valid = row < H;
-  cd v[16];
+  const int ti = line + R;  // tile row of this output row
+  const int c0 = 16 * t;    // this thread's contiguous span [c0, c0+16)
+  cd f[16];
+  if (DK == DN_MEDIAN3) {
+    auto col = [&](int j) {
+      const int c = colwrap<LW>(c0 + j, W);
+      return sorted_col(ld_cd(s_work + tl.at(ti - 1, c)), ld_cd(s_work + tl.at(ti, c)),
+                        ld_cd(s_work + tl.at(ti + 1, c)));
+    };
+    Sorted3 A = col(-1), B = col(0);
 #pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    const int c = t + T * m;
-    v[m] = (valid && c < W) ? denoise_at(s_work, W, line + R, c, DK, ks, s_taps) : cd{0.0, 0.0};
+    for (int j = 0; j < 16; ++j) {
+      Sorted3 C = col(j + 1);
+      f[j] = median_cols(A, B, C);
+      A = B;
+      B = C;
+    }
+  } else if (DK == DN_CONV) {
+    const int r = ks >> 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      cd acc = cd{0.0, 0.0};
+      for (int ta = 0; ta < ks; ++ta) {
+        for (int tb = 0; tb < ks; ++tb) {
+          const double w = s_taps[ta * ks + tb];
+          const cd xx = ld_cd(s_work + tl.at(ti - (ta - r), colwrap<LW>(c0 + j - (tb - r), W)));
+          acc.x = fma(w, xx.x, acc.x);
+          acc.y = fma(w, xx.y, acc.y);
+        }
+      }
+      f[j] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = ld_cd(s_work + tl.at(ti, colwrap<LW>(c0 + j, W)));
   }
-  __syncthreads();
+  __syncthreads();  // tile no longer read: reuse it as the line buffer
   RowLayout lay{RowLayout::stride_for(W)};
-  fft_dispatch<LW, false>(v, s_work, s_tw, W, t, line, lay);
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (c0 + j < W) st_cd(s_work + lay.at(line, c0 + j), f[j]);
+  __syncthreads();
+  cd v[16];
+  if constexpr (LW > 0) {
+    line_fft_ct<LW, false, true>(v, s_work, s_tw, t, line, lay);
+  } else {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int c = t + T * m;
+      v[m] = c < W ? ld_cd(s_work + lay.at(line, c)) : cd{0.0, 0.0};
+    }
+    __syncthreads();
+    line_fft<false>(v, s_work, s_tw, W, t, line, lay);
+  }
   if (valid) {
     cd* zr = a.Z + ((long long)p * H + row) * W;
 #pragma unroll
@@ -162,9 +274,10 @@ __global__ void __launch_bounds__(256) k_col(ColArgs a) {
   const int H = LH > 0 ? LH : a.H;
   const int W = a.W;
   const int T = LH > 0 ? LH / 16 : threads_per_line(H);
+  const int ntw = LH > 0 ? tw_stage_size(LH) : H;
   cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(H * sizeof(cd)));
-  load_twiddles(s_tw, a.tw, H);
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)));
+  load_twiddles(s_tw, LH > 0 ? a.tws : a.tw, ntw);
   const int line = threadIdx.x % a.lpc, t = threadIdx.x / a.lpc;
   const int col = blockIdx.x * a.lpc + line;
   const bool valid = col < W;
@@ -225,11 +338,12 @@ __global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
   const int H = a.H;
   const int T = LW > 0 ? LW / 16 : threads_per_line(W);
   const long long N = (long long)H * W;
+  const int ntw = LW > 0 ? tw_stage_size(LW) : W;
   cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(W * sizeof(cd)));
-  double* s_red = reinterpret_cast<double*>(f_smem + al16f(W * sizeof(cd)) +
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)));
+  double* s_red = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)) +
                                             (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
-  load_twiddles(s_tw, a.tw, W);
+  load_twiddles(s_tw, LW > 0 ? a.tws : a.tw, ntw);
   const int line = threadIdx.x / T, t = threadIdx.x - line * T;
   const int row = blockIdx.x * a.lpc + line;
   const bool valid = row < H;

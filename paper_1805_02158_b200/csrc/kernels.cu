@@ -397,7 +397,30 @@ __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
   double acc[NG];
 #pragma unroll
   for (int i = 0; i < NG; ++i) acc[i] = 0.0;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
+  // pairs of pixels with 16-byte loads (every slot starts 16-byte aligned when N is even)
+  const long long N2 = (a.N & 1) ? 0 : (a.N >> 1);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N2;
+       p += (long long)gridDim.x * blockDim.x) {
+    double d0[KP1], d1[KP1];
+    double2 prev = __ldg(reinterpret_cast<const double2*>(w[0]) + p);
+#pragma unroll
+    for (int j = 0; j < KP1; ++j) {
+      const double2 nx = __ldg(reinterpret_cast<const double2*>(w[j + 1]) + p);
+      d0[j] = nx.x - prev.x;
+      d1[j] = nx.y - prev.y;
+      prev = nx;
+    }
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < KP1; ++i)
+#pragma unroll
+      for (int j = i; j < KP1; ++j) {
+        acc[q] = fma(d0[i], d0[j], acc[q]);
+        acc[q] = fma(d1[i], d1[j], acc[q]);
+        ++q;
+      }
+  }
+  for (long long p = 2 * N2 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
        p += (long long)gridDim.x * blockDim.x) {
     double d[KP1];
     double prev = __ldg(w[0] + p);
@@ -564,6 +587,47 @@ void launch_mgs(const VeArgs& a, cudaStream_t s) { k_mgs<<<a.B, 512, 0, s>>>(a);
 // --------------------------------------------------------------- VE: combine
 // x = x_m + sum_{j<k} xi_j (x_{m+j+1} - x_{m+j})  written over the cycle-start
 // slot; accepted only if finite (solvers.py:368-378).
+template <int KE>
+__device__ __forceinline__ double combine_span(const VeArgs& a, int b, int s0, double* out,
+                                               const double* xi_s) {
+  const double* w[KE + 1];
+  double xi[KE];
+#pragma unroll
+  for (int j = 0; j <= KE; ++j) w[j] = slot_ptr(a, b, s0 + j);
+#pragma unroll
+  for (int j = 0; j < KE; ++j) xi[j] = xi_s[j];
+  double nf = 0.0;
+  const long long N2 = (a.N & 1) ? 0 : (a.N >> 1);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N2;
+       p += (long long)gridDim.x * blockDim.x) {
+    double2 prev = reinterpret_cast<const double2*>(w[0])[p];
+    double2 acc = prev;
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      const double2 nx = reinterpret_cast<const double2*>(w[j + 1])[p];
+      acc.x = fma(xi[j], nx.x - prev.x, acc.x);
+      acc.y = fma(xi[j], nx.y - prev.y, acc.y);
+      prev = nx;
+    }
+    reinterpret_cast<double2*>(out)[p] = acc;
+    nf += (isfinite(acc.x) ? 0.0 : 1.0) + (isfinite(acc.y) ? 0.0 : 1.0);
+  }
+  for (long long p = 2 * N2 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
+       p += (long long)gridDim.x * blockDim.x) {
+    double prev = w[0][p];
+    double acc = prev;
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      const double nx = w[j + 1][p];
+      acc = fma(xi[j], nx - prev, acc);
+      prev = nx;
+    }
+    out[p] = acc;
+    nf += isfinite(acc) ? 0.0 : 1.0;
+  }
+  return nf;
+}
+
 __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   const int b = blockIdx.y;
   ImgState& s = a.st[b];
@@ -585,21 +649,20 @@ __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   if (threadIdx.x < ke) s_xi[threadIdx.x] = s.ve_xi[threadIdx.x];
   __syncthreads();
   const int s0 = s.start + a.m;
-  const double* w[MAXKP1 + 1];
-  for (int j = 0; j <= ke; ++j) w[j] = slot_ptr(a, b, s0 + j);
   double* out = a.ring + (long long)b * a.img_stride + (long long)s.start * a.slot_stride;
-  double nf[1] = {0.0};
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
-       p += (long long)gridDim.x * blockDim.x) {
-    double prev = w[0][p];
-    double acc = prev;
-    for (int j = 0; j < ke; ++j) {
-      double nx = w[j + 1][p];
-      acc = fma(s_xi[j], nx - prev, acc);
-      prev = nx;
-    }
-    out[p] = acc;
-    nf[0] += isfinite(acc) ? 0.0 : 1.0;
+  double nf[1];
+  switch (ke) {
+    case 1: nf[0] = combine_span<1>(a, b, s0, out, s_xi); break;
+    case 2: nf[0] = combine_span<2>(a, b, s0, out, s_xi); break;
+    case 3: nf[0] = combine_span<3>(a, b, s0, out, s_xi); break;
+    case 4: nf[0] = combine_span<4>(a, b, s0, out, s_xi); break;
+    case 5: nf[0] = combine_span<5>(a, b, s0, out, s_xi); break;
+    case 6: nf[0] = combine_span<6>(a, b, s0, out, s_xi); break;
+    case 7: nf[0] = combine_span<7>(a, b, s0, out, s_xi); break;
+    case 8: nf[0] = combine_span<8>(a, b, s0, out, s_xi); break;
+    case 9: nf[0] = combine_span<9>(a, b, s0, out, s_xi); break;
+    case 10: nf[0] = combine_span<10>(a, b, s0, out, s_xi); break;
+    default: nf[0] = combine_span<11>(a, b, s0, out, s_xi); break;
   }
   block_sum<1>(nf, s_red);
   const int nblk = gridDim.x;

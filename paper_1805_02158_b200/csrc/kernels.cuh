@@ -13,7 +13,8 @@ struct RowFwdArgs {
   View xin;
   DenoiseArgs dn;
   cd* Z;
-  const cd* tw;
+  const cd* tw;   // W_L^m, m < L (runtime plans)
+  const cd* tws;  // stage-major table (compile-time plans), tw_stage_size(L)
   const ImgState* st;
   int phase;
 };
@@ -21,7 +22,8 @@ struct RowFwdArgs {
 struct ColArgs {
   int B, H, W, lpc;
   cd* Z;
-  const cd* tw;
+  const cd* tw;   // W_L^m, m < L (runtime plans)
+  const cd* tws;  // stage-major table (compile-time plans), tw_stage_size(L)
   const double* g;
   double scale;
   const ImgState* st;
@@ -31,7 +33,8 @@ struct ColArgs {
 struct RowInvArgs {
   int B, H, W, lpc;
   const cd* Z;
-  const cd* tw;
+  const cd* tw;   // W_L^m, m < L (runtime plans)
+  const cd* tws;  // stage-major table (compile-time plans), tw_stage_size(L)
   View out;
   const double* base;  // x_b [B][H*W] (added) or null
   View xprev;          // epilogue: previous iterate
@@ -88,6 +91,7 @@ struct VeArgs {
 // launchers (kernels.cu)
 int configure_kernels();  // returns a cudaError_t
 void launch_twiddles(cd* tw, int L, cudaStream_t s);
+void launch_stage_twiddles(cd* tws, int L, cudaStream_t s);  // power-of-two L >= 16
 void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, double sigma,
                       double alpha, cudaStream_t s);
 size_t row_fwd_smem(int W, int lpc, int radius, int ksize);
