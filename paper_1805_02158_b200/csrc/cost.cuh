@@ -1,0 +1,90 @@
+// Shared helpers for the fused objective evaluation (cost.cu, fourier.cu).
+#pragma once
+
+#include "denoise.cuh"
+
+namespace redve {
+
+// Padded tile: element (i, c) at i*stride + c + c/16 -- conflict-free for the
+// contiguous 16-column spans each thread reads.
+struct TileLayout {
+  int stride;
+  __device__ __forceinline__ int at(int i, int c) const { return i * stride + c + (c >> 4); }
+  static REDVE_HD int stride_for(int W) { return W + (W >> 4) + 1; }
+};
+
+// c within [-radius, W + radius): wrap with one compare (no integer division).
+__device__ __forceinline__ int edge_wrap(int c, int W) {
+  return c < 0 ? c + W : (c >= W ? c - W : c);
+}
+
+struct Sorted3 {
+  cd lo, mid, hi;
+};
+__device__ __forceinline__ void sort2c(cd& a, cd& b) {
+  sort2(a.x, b.x);
+  sort2(a.y, b.y);
+}
+__device__ __forceinline__ Sorted3 sorted_col(cd a, cd b, cd c) {
+  sort2c(a, b);
+  sort2c(b, c);
+  sort2c(a, b);
+  return Sorted3{a, b, c};
+}
+__device__ __forceinline__ double med3d(double a, double b, double c) {
+  return fmax(fmin(a, b), fmin(fmax(a, b), c));
+}
+// Median of the 3x3 block whose columns are A, B, C (each sorted): exact
+// selection  med3( max(lows), med3(mids), min(highs) )  -- 2x fewer
+// comparisons than the 19-comparator network when columns are shared.
+__device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, const Sorted3& C) {
+  cd r;
+  r.x = med3d(fmax(fmax(A.lo.x, B.lo.x), C.lo.x), med3d(A.mid.x, B.mid.x, C.mid.x),
+              fmin(fmin(A.hi.x, B.hi.x), C.hi.x));
+  r.y = med3d(fmax(fmax(A.lo.y, B.lo.y), C.lo.y), med3d(A.mid.y, B.mid.y, C.mid.y),
+              fmin(fmin(A.hi.y, B.hi.y), C.hi.y));
+  return r;
+}
+
+// f over the 16 contiguous columns [c0, c0+16) of tile row ti (pairs).
+// WRAP(c) maps a column in [-r, W + r) into [0, W).
+template <int DK, class Wrap>
+__device__ __forceinline__ void denoise_span(cd (&f)[16], const cd* tile, const TileLayout& tl,
+                                             int ti, int c0, int ksize, const double* taps,
+                                             Wrap wrapc) {
+  if (DK == DN_MEDIAN3) {
+    auto col = [&](int j) {
+      const int c = wrapc(c0 + j);
+      return sorted_col(ld_cd(tile + tl.at(ti - 1, c)), ld_cd(tile + tl.at(ti, c)),
+                        ld_cd(tile + tl.at(ti + 1, c)));
+    };
+    Sorted3 A = col(-1), B = col(0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      Sorted3 C = col(j + 1);
+      f[j] = median_cols(A, B, C);
+      A = B;
+      B = C;
+    }
+  } else if (DK == DN_CONV) {
+    const int r = ksize >> 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      cd acc = cd{0.0, 0.0};
+      for (int ta = 0; ta < ksize; ++ta) {
+        for (int tb = 0; tb < ksize; ++tb) {
+          const double w = taps[ta * ksize + tb];
+          const cd xx = ld_cd(tile + tl.at(ti - (ta - r), wrapc(c0 + j - (tb - r))));
+          acc.x = fma(w, xx.x, acc.x);
+          acc.y = fma(w, xx.y, acc.y);
+        }
+      }
+      f[j] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = ld_cd(tile + tl.at(ti, wrapc(c0 + j)));
+  }
+}
+
+}  // namespace redve

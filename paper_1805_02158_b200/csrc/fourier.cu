@@ -14,6 +14,7 @@
 //
 // Sizes that are powers of two in [16, 1024] use compile-time FFT plans;
 // anything else the runtime plan (direct DFT for non powers of two).
+#include "cost.cuh"
 #include "kernels.cuh"
 
 namespace redve {
@@ -72,44 +73,10 @@ __device__ __forceinline__ void fft_dispatch(cd (&v)[16], cd* sm, const cd* tw, 
 }
 
 // --------------------------------------------------------------- row forward
-// Padded tile: element (i, c) at i*stride + c + c/16 -- conflict-free for the
-// contiguous 16-column spans each thread reads.
-struct TileLayout {
-  int stride;
-  __device__ __forceinline__ int at(int i, int c) const { return i * stride + c + (c >> 4); }
-};
-
 template <int LW>
 __device__ __forceinline__ int colwrap(int c, int W) {
-  if constexpr (LW > 0) return c < 0 ? c + W : (c >= W ? c - W : c);  // |c - [0,W)| <= radius
+  if constexpr (LW > 0) return edge_wrap(c, W);  // |c - [0,W)| <= radius
   else return wrap(c, W);
-}
-
-struct Sorted3 {
-  cd lo, mid, hi;
-};
-__device__ __forceinline__ void sort2c(cd& a, cd& b) {
-  sort2(a.x, b.x);
-  sort2(a.y, b.y);
-}
-__device__ __forceinline__ Sorted3 sorted_col(cd a, cd b, cd c) {
-  sort2c(a, b);
-  sort2c(b, c);
-  sort2c(a, b);
-  return Sorted3{a, b, c};
-}
-__device__ __forceinline__ double med3d(double a, double b, double c) {
-  return fmax(fmin(a, b), fmin(fmax(a, b), c));
-}
-// median of the 3x3 block whose columns are A, B, C (each sorted): exact
-// selection  med3( max(lows), med3(mids), min(highs) ).
-__device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, const Sorted3& C) {
-  cd r;
-  r.x = med3d(fmax(fmax(A.lo.x, B.lo.x), C.lo.x), med3d(A.mid.x, B.mid.x, C.mid.x),
-              fmin(fmin(A.hi.x, B.hi.x), C.hi.x));
-  r.y = med3d(fmax(fmax(A.lo.y, B.lo.y), C.lo.y), med3d(A.mid.y, B.mid.y, C.mid.y),
-              fmin(fmin(A.hi.y, B.hi.y), C.hi.y));
-  return r;
 }
 
 template <int LW, int DK>
@@ -139,13 +106,27 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   // tile rows r0-R .. r0+lpc+R-1 (periodic), both images
   if ((W & 1) == 0) {  // even width: every row (and image) starts 16-byte aligned
     const int W2 = W >> 1;
-    for (int idx = threadIdx.x; idx < trows * W2; idx += blockDim.x) {
-      const int i = idx / W2, c2 = idx - i * W2;
-      const long long o = (long long)wrap(r0 - R + i, H) * W + 2 * c2;
-      double2 u0 = x0 ? __ldg(reinterpret_cast<const double2*>(x0 + o)) : make_double2(0.0, 0.0);
-      double2 u1 = x1 ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
-      st_cd(s_work + tl.at(i, 2 * c2), cd{u0.x, u1.x});
-      st_cd(s_work + tl.at(i, 2 * c2 + 1), cd{u0.y, u1.y});
+    const int total = trows * W2;
+    // batches of 4 iterations: the 8 loads of a batch issue before its stores
+    for (int base = 0; base < total; base += 4 * blockDim.x) {
+      double2 u0[4], u1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base + q * blockDim.x + threadIdx.x;
+        const int i = idx / W2, c2 = idx - i * W2;
+        const long long o = (long long)wrap(r0 - R + i, H) * W + 2 * c2;
+        const bool in = idx < total;
+        u0[q] = (in && x0) ? __ldg(reinterpret_cast<const double2*>(x0 + o)) : make_double2(0.0, 0.0);
+        u1[q] = (in && x1) ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = base + q * blockDim.x + threadIdx.x;
+        if (idx >= total) break;
+        const int i = idx / W2, c2 = idx - i * W2;
+        st_cd(s_work + tl.at(i, 2 * c2), cd{u0[q].x, u1[q].x});
+        st_cd(s_work + tl.at(i, 2 * c2 + 1), cd{u0[q].y, u1[q].y});
+      }
     }
   } else {
     for (int idx = threadIdx.x; idx < trows * W; idx += blockDim.x) {
@@ -161,39 +142,7 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int ti = line + R;  // tile row of this output row
   const int c0 = 16 * t;    // this thread's contiguous span [c0, c0+16)
   cd f[16];
-  if (DK == DN_MEDIAN3) {
-    auto col = [&](int j) {
-      const int c = colwrap<LW>(c0 + j, W);
-      return sorted_col(ld_cd(s_work + tl.at(ti - 1, c)), ld_cd(s_work + tl.at(ti, c)),
-                        ld_cd(s_work + tl.at(ti + 1, c)));
-    };
-    Sorted3 A = col(-1), B = col(0);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      Sorted3 C = col(j + 1);
-      f[j] = median_cols(A, B, C);
-      A = B;
-      B = C;
-    }
-  } else if (DK == DN_CONV) {
-    const int r = ks >> 1;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      cd acc = cd{0.0, 0.0};
-      for (int ta = 0; ta < ks; ++ta) {
-        for (int tb = 0; tb < ks; ++tb) {
-          const double w = s_taps[ta * ks + tb];
-          const cd xx = ld_cd(s_work + tl.at(ti - (ta - r), colwrap<LW>(c0 + j - (tb - r), W)));
-          acc.x = fma(w, xx.x, acc.x);
-          acc.y = fma(w, xx.y, acc.y);
-        }
-      }
-      f[j] = acc;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) f[j] = ld_cd(s_work + tl.at(ti, colwrap<LW>(c0 + j, W)));
-  }
+  denoise_span<DK>(f, s_work, tl, ti, c0, ks, s_taps, [&](int c) { return colwrap<LW>(c, W); });
   __syncthreads();  // tile no longer read: reuse it as the line buffer
   RowLayout lay{RowLayout::stride_for(W)};
 #pragma unroll
@@ -366,28 +315,43 @@ __global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
     const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) + (long long)row * W : nullptr;
     const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N + (long long)row * W : nullptr;
     const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N + (long long)row * W : nullptr;
+    // two batches of 8 columns: all loads of a batch issue before its stores
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int c = t + T * m;
-      if (c >= W) continue;
-      if (o0) {
-        const double val = v[m].x + (bs0 ? __ldg(bs0 + c) : 0.0);
-        o0[c] = val;
-        if (p0) {
-          const double xp = __ldg(p0 + c), d = val - xp;
-          acc[0] = fma(d, d, acc[0]);
-          acc[1] = fma(xp, xp, acc[1]);
-          acc[2] += isfinite(val) ? 0.0 : 1.0;
-        }
+    for (int h = 0; h < 2; ++h) {
+      double lb0[8], lb1[8], lp0[8], lp1[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = t + T * (8 * h + q);
+        const bool in = c < W;
+        lb0[q] = (in && bs0) ? __ldg(bs0 + c) : 0.0;
+        lb1[q] = (in && bs1) ? __ldg(bs1 + c) : 0.0;
+        lp0[q] = (in && p0) ? __ldg(p0 + c) : 0.0;
+        lp1[q] = (in && p1) ? __ldg(p1 + c) : 0.0;
       }
-      if (o1) {
-        const double val = v[m].y + (bs1 ? __ldg(bs1 + c) : 0.0);
-        o1[c] = val;
-        if (p1) {
-          const double xp = __ldg(p1 + c), d = val - xp;
-          acc[3] = fma(d, d, acc[3]);
-          acc[4] = fma(xp, xp, acc[4]);
-          acc[5] += isfinite(val) ? 0.0 : 1.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int m = 8 * h + q;
+        const int c = t + T * m;
+        if (c >= W) continue;
+        if (o0) {
+          const double val = v[m].x + lb0[q];
+          o0[c] = val;
+          if (p0) {
+            const double d = val - lp0[q];
+            acc[0] = fma(d, d, acc[0]);
+            acc[1] = fma(lp0[q], lp0[q], acc[1]);
+            acc[2] += isfinite(val) ? 0.0 : 1.0;
+          }
+        }
+        if (o1) {
+          const double val = v[m].y + lb1[q];
+          o1[c] = val;
+          if (p1) {
+            const double d = val - lp1[q];
+            acc[3] = fma(d, d, acc[3]);
+            acc[4] = fma(lp1[q], lp1[q], acc[4]);
+            acc[5] += isfinite(val) ? 0.0 : 1.0;
+          }
         }
       }
     }

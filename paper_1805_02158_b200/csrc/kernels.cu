@@ -97,51 +97,6 @@ static inline __host__ __device__ size_t al16(size_t b) { return (b + 15) & ~siz
 // PSNR = 10 log10(255^2 / mse)                          (imaging.py:234-248)
 // Modes: record on the logging cadence (solvers.py:232-238, best-iterate
 // tracking :235-236), note_initial (:219-223), finalize (:255-262).
-__device__ double psnr_from(double ssd, long long n) {
-  double mse = ssd / (double)n;
-  if (mse == 0.0) return INFINITY;
-  if (!isfinite(mse)) return -INFINITY;
-  return 10.0 * log10(255.0 * 255.0 / mse);
-}
-
-__device__ void cost_finish(ImgState& s, int b, double fid, double reg, double ssd, bool has_ref,
-                            const CostArgs& a) {
-  const double cost = fid / (2.0 * a.sigma * a.sigma) + a.alpha * (0.5 * reg);
-  const long long N = (long long)a.H * a.W;
-  if (a.mode == COST_INIT) {
-    if (isfinite(cost)) {
-      s.best_cost = cost;
-      s.copy_best = 1;
-      s.has_best = 1;
-    } else {
-      s.copy_best = 0;
-    }
-    return;
-  }
-  if (a.mode == COST_FINAL) {
-    s.use_best = (s.has_best && !(isfinite(cost) && cost <= s.best_cost)) ? 1 : 0;
-    return;
-  }
-  const long long i = (long long)b * a.tr.cap + (s.k - 1);
-  if (s.k - 1 < a.tr.cap) {
-    a.tr.cost[i] = cost;
-    if (has_ref) a.tr.psnr[i] = psnr_from(ssd, N);
-  }
-  s.copy_best = 0;
-  if (a.ctl.track_best && cost < s.best_cost) {
-    s.best_cost = cost;
-    s.copy_best = 1;
-    s.has_best = 1;
-  }
-  if (!isfinite(cost) && s.err == ERR_NONE) s.err = ERR_NONFINITE_COST;
-}
-
-__device__ __forceinline__ bool cost_wants(const ImgState& s, const CostArgs& a) {
-  if (a.mode == COST_RECORD) return s.stepped && (s.k % a.ctl.log_every == 0);
-  if (a.mode == COST_INIT || a.mode == COST_VALUE) return true;
-  return s.err == ERR_NONE;  // final
-}
-
 template <int DK>
 __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
@@ -320,6 +275,10 @@ static void cost_t(const CostArgs& a, int npairs, cudaStream_t s) {
   k_cost<DK><<<grid, 256, sm, s>>>(a);
 }
 void launch_cost(const CostArgs& a, int npairs, cudaStream_t s) {
+  if (cost_fast_ok(a)) {
+    launch_cost_fast(a, npairs, s);
+    return;
+  }
   switch (a.dn.kind) {
     case DN_CONV: cost_t<DN_CONV>(a, npairs, s); break;
     case DN_MEDIAN3: cost_t<DN_MEDIAN3>(a, npairs, s); break;

@@ -72,6 +72,52 @@ struct CostArgs {
   unsigned* counters;
 };
 
+__device__ inline double psnr_from(double ssd, long long n) {
+  double mse = ssd / (double)n;
+  if (mse == 0.0) return INFINITY;
+  if (!isfinite(mse)) return -INFINITY;
+  return 10.0 * log10(255.0 * 255.0 / mse);
+}
+
+__device__ inline void cost_finish(ImgState& s, int b, double fid, double reg, double ssd, bool has_ref,
+                            const CostArgs& a) {
+  const double cost = fid / (2.0 * a.sigma * a.sigma) + a.alpha * (0.5 * reg);
+  const long long N = (long long)a.H * a.W;
+  if (a.mode == COST_INIT) {
+    if (isfinite(cost)) {
+      s.best_cost = cost;
+      s.copy_best = 1;
+      s.has_best = 1;
+    } else {
+      s.copy_best = 0;
+    }
+    return;
+  }
+  if (a.mode == COST_FINAL) {
+    s.use_best = (s.has_best && !(isfinite(cost) && cost <= s.best_cost)) ? 1 : 0;
+    return;
+  }
+  const long long i = (long long)b * a.tr.cap + (s.k - 1);
+  if (s.k - 1 < a.tr.cap) {
+    a.tr.cost[i] = cost;
+    if (has_ref) a.tr.psnr[i] = psnr_from(ssd, N);
+  }
+  s.copy_best = 0;
+  if (a.ctl.track_best && cost < s.best_cost) {
+    s.best_cost = cost;
+    s.copy_best = 1;
+    s.has_best = 1;
+  }
+  if (!isfinite(cost) && s.err == ERR_NONE) s.err = ERR_NONFINITE_COST;
+}
+
+__device__ __forceinline__ bool cost_wants(const ImgState& s, const CostArgs& a) {
+  if (a.mode == COST_RECORD) return s.stepped && (s.k % a.ctl.log_every == 0);
+  if (a.mode == COST_INIT || a.mode == COST_VALUE) return true;
+  return s.err == ERR_NONE;  // final
+}
+
+
 struct VeArgs {
   int B;
   long long N;
@@ -102,6 +148,8 @@ void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
 void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);
 int cost_rows(int H);
 void launch_cost(const CostArgs& a, int npairs, cudaStream_t s);
+bool cost_fast_ok(const CostArgs& a);
+void launch_cost_fast(const CostArgs& a, int npairs, cudaStream_t s);
 void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
                       cudaStream_t s);
 void launch_gram(const VeArgs& a, cudaStream_t s);
