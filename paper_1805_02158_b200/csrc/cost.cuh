@@ -32,17 +32,17 @@ __device__ __forceinline__ Sorted3 sorted_col(cd a, cd b, cd c) {
   return Sorted3{a, b, c};
 }
 __device__ __forceinline__ double med3d(double a, double b, double c) {
-  return fmax(fmin(a, b), fmin(fmax(a, b), c));
+  return dmax(dmin(a, b), dmin(dmax(a, b), c));
 }
 // Median of the 3x3 block whose columns are A, B, C (each sorted): exact
 // selection  med3( max(lows), med3(mids), min(highs) )  -- 2x fewer
 // comparisons than the 19-comparator network when columns are shared.
 __device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, const Sorted3& C) {
   cd r;
-  r.x = med3d(fmax(fmax(A.lo.x, B.lo.x), C.lo.x), med3d(A.mid.x, B.mid.x, C.mid.x),
-              fmin(fmin(A.hi.x, B.hi.x), C.hi.x));
-  r.y = med3d(fmax(fmax(A.lo.y, B.lo.y), C.lo.y), med3d(A.mid.y, B.mid.y, C.mid.y),
-              fmin(fmin(A.hi.y, B.hi.y), C.hi.y));
+  r.x = med3d(dmax(dmax(A.lo.x, B.lo.x), C.lo.x), med3d(A.mid.x, B.mid.x, C.mid.x),
+              dmin(dmin(A.hi.x, B.hi.x), C.hi.x));
+  r.y = med3d(dmax(dmax(A.lo.y, B.lo.y), C.lo.y), med3d(A.mid.y, B.mid.y, C.mid.y),
+              dmin(dmin(A.hi.y, B.hi.y), C.hi.y));
   return r;
 }
 

@@ -22,11 +22,16 @@ struct DenoiseArgs {
   const double* taps; // device, ksize*ksize, row-major taps[a][b]
 };
 
+// One comparison, two selects (fmin/fmax cost two compares plus NaN fix-ups on
+// sm_100; iterates reaching a denoiser are finite, so plain ordering is exact).
 __device__ __forceinline__ void sort2(double& a, double& b) {
-  double lo = fmin(a, b), hi = fmax(a, b);
+  const bool sw = b < a;
+  const double lo = sw ? b : a, hi = sw ? a : b;
   a = lo;
   b = hi;
 }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 
 // Median of 9 with the 19-comparator network (exact selection).
 __device__ __forceinline__ double median9(double* p) {

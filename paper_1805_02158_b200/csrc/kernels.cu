@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
   for (int i = 0; i < NG; ++i) acc[i] = 0.0;
   // pairs of pixels with 16-byte loads (every slot starts 16-byte aligned when N is even)
   const long long N2 = (a.N & 1) ? 0 : (a.N >> 1);
+#pragma unroll 2
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N2;
        p += (long long)gridDim.x * blockDim.x) {
     double d0[KP1], d1[KP1];
@@ -557,6 +558,7 @@ __device__ __forceinline__ double combine_span(const VeArgs& a, int b, int s0, d
   for (int j = 0; j < KE; ++j) xi[j] = xi_s[j];
   double nf = 0.0;
   const long long N2 = (a.N & 1) ? 0 : (a.N >> 1);
+#pragma unroll 2
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N2;
        p += (long long)gridDim.x * blockDim.x) {
     double2 prev = reinterpret_cast<const double2*>(w[0])[p];
