@@ -33,7 +33,10 @@ size_t row_fwd_smem(int W, int lpc, int radius, int ksize) {
   return tw_bytes(W) + al16f((size_t)ksize * ksize * sizeof(double)) +
          (tile > lines ? tile : lines);
 }
-size_t col_smem(int H, int lpc) { return tw_bytes(H) + (size_t)H * lpc * sizeof(cd); }
+size_t col_smem(int H, int lpc) {
+  const int T = threads_per_line(H);
+  return tw_bytes(H) + (size_t)H * lpc * sizeof(cd) + (size_t)16 * T * lpc * sizeof(double);
+}
 size_t row_inv_smem(int W, int lpc) {
   return tw_bytes(W) + (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) +
          al16f(32 * 6 * sizeof(double));
@@ -231,6 +234,20 @@ __global__ void __launch_bounds__(256) k_col(ColArgs a) {
   const int col = blockIdx.x * a.lpc + line;
   const bool valid = col < W;
   cd* zc = a.Z + (long long)p * H * W + (valid ? col : 0);
+  // the spectral multiplier for this thread's 16 elements: async copies into
+  // shared memory now, consumed after the forward transform
+  double* s_g = reinterpret_cast<double*>(s_work + (size_t)H * a.lpc);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int r = t + T * m;
+    if (valid && r < H) {
+      const unsigned dst =
+          (unsigned)__cvta_generic_to_shared(s_g + m * blockDim.x + threadIdx.x);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                   "l"(a.g + (long long)r * W + col));
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
   cd v[16];
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
@@ -240,10 +257,11 @@ __global__ void __launch_bounds__(256) k_col(ColArgs a) {
   __syncthreads();
   ColLayout lay{a.lpc};
   fft_dispatch<LH, false>(v, s_work, s_tw, H, t, line, lay);
+  asm volatile("cp.async.wait_group 0;\n" ::);  // this thread's own copies
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
     const int r = t + T * m;
-    if (valid && r < H) v[m] = v[m] * (a.scale * __ldg(a.g + (long long)r * W + col));
+    if (valid && r < H) v[m] = v[m] * (a.scale * s_g[m * blockDim.x + threadIdx.x]);
   }
   fft_dispatch<LH, true>(v, s_work, s_tw, H, t, line, lay);
   if (valid) {
