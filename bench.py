@@ -290,15 +290,24 @@ def run_native(a):
             "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
             "traffic": ncu_traffic(dom)}
 
-    # ---- e2e through the public API with host buffers
+    # ---- e2e through the public API with host buffers (pinned, allocated up front):
+    # problem setup from the host measurements, H2D of y and x0, the solve, D2H of
+    # the solutions (traces come back inside solve_batch)
+    ys_host = torch.from_numpy(ys).pin_memory()
+    x_host = torch.empty_like(ys_host).pin_memory()
     e2e_steps = max(1, min(a.steps, 3))
+    b2 = rv.RedBatch(op, ys_host, SIGMA, ALPHA, rv.Median3())  # warm the buffer cache
+    rv.solve_batch(b2, ys_host, cfg)
+    del b2
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        b2 = rv.RedBatch(op, ys, SIGMA, ALPHA, rv.Median3())
-        X, traces = rv.solve_batch(b2, ys, cfg)
-        Xh = X.cpu().numpy()
+        b2 = rv.RedBatch(op, ys_host, SIGMA, ALPHA, rv.Median3())
+        X, traces = rv.solve_batch(b2, ys_host, cfg)
+        x_host.copy_(X)
+        del b2
+    Xh = x_host.numpy()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")

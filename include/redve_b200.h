@@ -138,6 +138,8 @@ const char* redve_last_error(const redve_ctx* ctx);
 int redve_set_stream(redve_ctx* ctx, void* cuda_stream); /* cudaStream_t, 0 = legacy default */
 int redve_synchronize(redve_ctx* ctx);
 const char* redve_version(void);
+/* return the library's cached device blocks to the driver */
+void redve_release_cached_memory(void);
 /* total kernels this library has launched (all contexts) */
 uint64_t redve_kernel_launches(void);
 /* time every kernel with CUDA events on the context's stream (measurement aid) */

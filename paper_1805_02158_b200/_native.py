@@ -72,6 +72,7 @@ class VeResultC(C.Structure):
 SYMBOLS = {
     "redve_version": (C.c_char_p, []),
     "redve_kernel_launches": (C.c_uint64, []),
+    "redve_release_cached_memory": (None, []),
     "redve_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "redve_profile_report": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _dp, C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int)]),

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -15,19 +16,68 @@
 
 using namespace redve;
 
+// Device-memory cache: problems are created per solve by the drop-in API, so
+// their buffers (ring, spectra, traces ...) are recycled instead of going
+// through cudaMalloc/cudaFree (which synchronise the device) every time.
+struct MemPool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;  // (device, bytes) -> ptr
+  static size_t round(size_t b) {
+    const size_t g = b >= (1u << 20) ? (1u << 20) : 4096;
+    return (b + g - 1) / g * g;
+  }
+  cudaError_t get(void** p, size_t bytes, size_t* got) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.lower_bound({dev, bytes});
+      if (it != free_blocks.end() && it->first.first == dev && it->first.second <= 2 * bytes) {
+        *p = it->second;
+        *got = it->first.second;
+        free_blocks.erase(it);
+        return cudaSuccess;
+      }
+    }
+    *got = bytes;
+    return cudaMalloc(p, bytes);
+  }
+  void put(void* p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    free_blocks.insert({{dev, bytes}, p});
+  }
+  void release() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    free_blocks.clear();
+  }
+};
+static MemPool g_pool;
+
 struct DevBuf {
   void* p = nullptr;
-  size_t n = 0;
+  size_t n = 0;   // usable bytes requested
+  size_t cap = 0; // bytes of the pooled block
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) g_pool.put(p, cap);
   }
   cudaError_t ensure(size_t bytes) {
-    if (bytes <= n && p) return cudaSuccess;
-    if (p) cudaFree(p);
+    if (bytes <= cap && p) {
+      n = bytes;
+      return cudaSuccess;
+    }
+    if (p) g_pool.put(p, cap);
     p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&p, bytes > 0 ? bytes : 16);
-    if (e == cudaSuccess) n = bytes;
+    n = cap = 0;
+    const size_t want = MemPool::round(bytes > 0 ? bytes : 16);
+    size_t got = 0;
+    cudaError_t e = g_pool.get(&p, want, &got);
+    if (e == cudaSuccess) {
+      n = bytes;
+      cap = got;
+    }
     return e;
   }
   template <class T>
@@ -239,6 +289,8 @@ extern "C" {
 const char* redve_version(void) { return "redve_b200 0.1.0 (sm_100a)"; }
 
 uint64_t redve_kernel_launches(void) { return g_launches.load(); }
+
+void redve_release_cached_memory(void) { g_pool.release(); }
 
 int redve_profile(redve_ctx* ctx, int enable) {
   ctx->profiling = enable != 0;
