@@ -152,6 +152,11 @@ int redve_profile_report(redve_ctx* ctx, int max_kinds, char* names, double* tot
 int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
                   const double* x, double* out);
 
+/* PatchWeighted.weight_maps (denoisers.py:83-111): the balanced map of every
+ * search offset, raster order; maps: DEVICE [B][(2 sr + 1)^2][H][W] */
+int redve_patch_weight_maps(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
+                            const double* x, double* maps);
+
 /* ---- operators: apply / adjoint (imaging.py Blur / BlurDownsample) -------- */
 int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
                          const double* x, double* out);

@@ -83,6 +83,8 @@ SYMBOLS = {
     "redve_synchronize": (C.c_int, [C.c_void_p]),
     "redve_denoise": (C.c_int, [C.c_void_p, C.POINTER(DenoiserDesc), C.c_int, C.c_int, C.c_int,
                                 C.c_void_p, C.c_void_p]),
+    "redve_patch_weight_maps": (C.c_int, [C.c_void_p, C.POINTER(DenoiserDesc), C.c_int, C.c_int,
+                                          C.c_int, C.c_void_p, C.c_void_p]),
     "redve_operator_apply": (C.c_int, [C.c_void_p, C.POINTER(OperatorDesc), C.c_int, C.c_int,
                                        C.c_int, C.c_void_p, C.c_void_p]),
     "redve_operator_adjoint": (C.c_int, [C.c_void_p, C.POINTER(OperatorDesc), C.c_int, C.c_int,

@@ -13,6 +13,7 @@
 
 #include "../../include/redve_b200.h"
 #include "kernels.cuh"
+#include "sr.cuh"
 
 using namespace redve;
 
@@ -209,6 +210,10 @@ struct redve_problem {
   int lpc_row, lpc_col;
   int separable = 0;
   DevBuf hsep;  // [u | v] when the PSF is rank one
+  int dn_api_kind = 0;  // REDVE_DN_* as requested
+  int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
+  double pw_h = 110.0;
+  DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
   DevBuf htaps, dntaps, y, ref, hty, xb, g, Z, state, partials, cnt_inv, cnt_cost, cnt_ve,
       fbuf, ring, best, q, trace, vals;
   bool has_ref = false;
@@ -282,6 +287,83 @@ static View plain(const double* base, long long N) {
   v.S = 1;
   v.mode = 0;
   return v;
+}
+
+// f(x) into p->fbuf for the device denoisers the Fourier kernels do not fuse
+// (PatchWeighted always; the stencils on the CG route).
+static int denoise_to_fbuf(redve_problem* p, View x, int phase) {
+  redve_ctx* ctx = p->ctx;
+  if (p->dn_api_kind == REDVE_DN_PATCH) {
+    PwArgs a;
+    a.B = p->B; a.H = p->H; a.W = p->W;
+    a.pr = p->pw_pr; a.sr = p->pw_sr; a.npos = p->pw_npos; a.iters = p->pw_iters;
+    a.inv_h2 = 1.0 / (p->pw_h * p->pw_h);
+    a.xin = x;
+    a.w0 = p->w0.as<double>(); a.D0 = p->D0.as<double>(); a.D1 = p->D1.as<double>();
+    a.out = p->fbuf.as<double>();
+    a.st = p->state.as<ImgState>(); a.phase = phase;
+    int n = 0;
+    RUN(ctx, "patch_weighted", launch_pw(a, ctx->stream, &n));
+    g_launches.fetch_add(n - 1);
+  } else {
+    RUN(ctx, "denoise", launch_denoise_view(x, dn_args(p), p->fbuf.as<double>(),
+                                            p->state.as<ImgState>(), phase, p->B, p->H, p->W,
+                                            ctx->stream));
+  }
+  CKL();
+  return REDVE_OK;
+}
+
+static int cg_any_active(redve_problem* p, std::vector<CgState>& h) {
+  redve_ctx* ctx = p->ctx;
+  h.resize(p->B);
+  CK(cudaMemcpyAsync(h.data(), p->cgst.p, sizeof(CgState) * p->B, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int b = 0; b < p->B; ++b)
+    if (h[b].active) return 1;
+  return 0;
+}
+
+// One CG fixed-point step (objective.py:105-121, scipy cg semantics) from xin
+// into xout; f_ext overrides the device denoiser (host plug-in).
+static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const double* f_ext) {
+  redve_ctx* ctx = p->ctx;
+  const cudaStream_t s = ctx->stream;
+  if (!f_ext) {
+    int r = denoise_to_fbuf(p, xin, phase);
+    if (r) return r;
+  }
+  CgArgs a;
+  a.B = p->B; a.H = p->H; a.W = p->W; a.factor = p->op.factor; a.k = p->op.ksize;
+  a.taps = p->htaps.as<double>();
+  a.inv_sigma2 = 1.0 / (p->sigma * p->sigma); a.alpha = p->alpha;
+  a.rtol = 1e-6; a.abort = 1e-4; a.maxiter = 200; a.it = 0;  // objective.py:35-37
+  a.xin = xin; a.xout = xout;
+  a.hty = p->hty.as<double>(); a.f = f_ext ? f_ext : p->fbuf.as<double>();
+  a.r = p->cr.as<double>(); a.p = p->cp.as<double>(); a.q = p->cq.as<double>();
+  a.cg = p->cgst.as<CgState>(); a.st = p->state.as<ImgState>(); a.phase = phase;
+  a.partials = p->part_cg.as<double>(); a.counters = p->cnt_cg.as<unsigned>();
+  RUN(ctx, "cg_init", launch_cg_init(a, s));
+  CKL();
+  std::vector<CgState> h;
+  for (int it = 0; it < a.maxiter; ++it) {
+    if (it % 2 == 0) {  // host check of the per-image stop flags every 2 iterations
+      int any = cg_any_active(p, h);
+      if (any > 1) return any;
+      if (!any) break;
+    }
+    a.it = it;
+    RUN(ctx, "cg_matvec", launch_cg_iter(a, s));
+    RUN(ctx, "cg_update", launch_cg_update(a, s));
+    CKL();
+  }
+  RUN(ctx, "cg_zero_b", launch_cg_zero_b(a, s));
+  CgArgs rres = a;
+  rres.xin = xout;
+  RUN(ctx, "cg_resid", launch_cg_resid(rres, s));
+  CKL();
+  return REDVE_OK;
 }
 
 extern "C" {
@@ -386,10 +468,64 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       CK(cudaStreamSynchronize(ctx->stream));
       return REDVE_OK;
     }
+    case REDVE_DN_PATCH: {
+      if (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1)
+        return fail(ctx, REDVE_E_VALUE,
+                    "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+      const int npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
+      CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
+      CK(ctx->scratch_a.ensure(sizeof(double) * N * B * npos));
+      CK(ctx->scratch_b.ensure(sizeof(double) * N * B * 2));
+      PwArgs a;
+      a.B = B; a.H = H; a.W = W;
+      a.pr = dn->patch_radius; a.sr = dn->search_radius; a.npos = npos;
+      a.iters = dn->balance_iters; a.inv_h2 = 1.0 / (dn->h * dn->h);
+      a.xin = plain(x, N);
+      a.w0 = ctx->scratch_a.as<double>();
+      a.D0 = ctx->scratch_b.as<double>();
+      a.D1 = ctx->scratch_b.as<double>() + N * B;
+      a.out = out;
+      a.st = ctx->ve_state.as<ImgState>();
+      a.phase = PH_SETUP;
+      int n = 0;
+      RUN(ctx, "patch_weighted", launch_pw(a, ctx->stream, &n));
+      g_launches.fetch_add(n - 1);
+      CKL();
+      return REDVE_OK;
+    }
     default:
       return fail(ctx, REDVE_E_UNSUPPORTED, "denoiser kind %d not available in this build",
                   dn->kind);
   }
+}
+
+int redve_patch_weight_maps(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
+                            const double* x, double* maps) {
+  if (dn->kind != REDVE_DN_PATCH) return fail(ctx, REDVE_E_VALUE, "not a PatchWeighted descriptor");
+  if (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1)
+    return fail(ctx, REDVE_E_VALUE,
+                "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+  const long long N = (long long)H * W;
+  const int npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
+  CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
+  CK(ctx->scratch_a.ensure(sizeof(double) * N * B * npos));
+  CK(ctx->scratch_b.ensure(sizeof(double) * N * B * 2));
+  PwArgs a;
+  a.B = B; a.H = H; a.W = W;
+  a.pr = dn->patch_radius; a.sr = dn->search_radius; a.npos = npos;
+  a.iters = dn->balance_iters; a.inv_h2 = 1.0 / (dn->h * dn->h);
+  a.xin = plain(x, N);
+  a.w0 = ctx->scratch_a.as<double>();
+  a.D0 = ctx->scratch_b.as<double>();
+  a.D1 = ctx->scratch_b.as<double>() + N * B;
+  a.out = nullptr;
+  a.st = ctx->ve_state.as<ImgState>();
+  a.phase = PH_SETUP;
+  int n = 0;
+  RUN(ctx, "patch_maps", launch_pw_maps(a, ctx->stream, &n, maps));
+  g_launches.fetch_add(n - 1);
+  CKL();
+  return REDVE_OK;
 }
 
 // ------------------------------------------------------------------ operators
@@ -459,15 +595,19 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     if (dn->ksize > H || dn->ksize > W)
       return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
   }
-  if (op->kind != REDVE_OP_BLUR)
-    return fail(ctx, REDVE_E_UNSUPPORTED, "BlurDownsample problems: CG path not built yet");
   if (dn->kind != REDVE_DN_IDENTITY && dn->kind != REDVE_DN_CONV && dn->kind != REDVE_DN_MEDIAN3 &&
-      dn->kind != REDVE_DN_EXTERNAL)
+      dn->kind != REDVE_DN_EXTERNAL && dn->kind != REDVE_DN_PATCH)
     return fail(ctx, REDVE_E_UNSUPPORTED, "denoiser kind %d not available in this build",
                 dn->kind);
-  if (H > 4096 || W > 4096) return fail(ctx, REDVE_E_UNSUPPORTED, "image side > 4096");
-  if (!is_pow2(H) && H > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
-  if (!is_pow2(W) && W > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
+  if (dn->kind == REDVE_DN_PATCH &&
+      (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1))
+    return fail(ctx, REDVE_E_VALUE,
+                "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+  if (op->kind == REDVE_OP_BLUR) {  // Fourier route limits
+    if (H > 4096 || W > 4096) return fail(ctx, REDVE_E_UNSUPPORTED, "image side > 4096");
+    if (!is_pow2(H) && H > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
+    if (!is_pow2(W) && W > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
+  }
 
   redve_problem* p = new redve_problem();
   p->ctx = ctx;
@@ -480,6 +620,14 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   p->Wy = (W + f - 1) / f;
   p->npairs = (B + 1) / 2;
   p->dn_kind = map_dn_kind(dn->kind);
+  p->dn_api_kind = dn->kind;
+  if (dn->kind == REDVE_DN_PATCH) {
+    p->pw_pr = dn->patch_radius;
+    p->pw_sr = dn->search_radius;
+    p->pw_iters = dn->balance_iters;
+    p->pw_h = dn->h;
+    p->pw_npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
+  }
   p->dn_ksize = dn->kind == REDVE_DN_CONV ? dn->ksize : 0;
   p->sigma = sigma;
   p->alpha = alpha;
@@ -555,8 +703,33 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   PK(cudaMemsetAsync(p->cnt_cost.p, 0, sizeof(unsigned) * (B + 1), s));
   PK(cudaMemsetAsync(p->cnt_ve.p, 0, sizeof(unsigned) * (B + 1), s));
   PK(p->vals.ensure(sizeof(double) * 3 * B));
+  // device denoiser output / PatchWeighted fields
+  if (dn->kind != REDVE_DN_EXTERNAL) PK(p->fbuf.ensure(sizeof(double) * p->N * B));
+  if (dn->kind == REDVE_DN_PATCH) {
+    PK(p->w0.ensure(sizeof(double) * p->N * B * p->pw_npos));
+    PK(p->D0.ensure(sizeof(double) * p->N * B));
+    PK(p->D1.ensure(sizeof(double) * p->N * B));
+  }
+  if (!p->fourier) {  // CG route
+    PK(p->cgst.ensure(sizeof(CgState) * B));
+    PK(p->cr.ensure(sizeof(double) * p->N * B));
+    PK(p->cp.ensure(sizeof(double) * p->N * B));
+    PK(p->cq.ensure(sizeof(double) * p->N * B));
+    PK(p->cnt_cg.ensure(sizeof(unsigned) * (B + 1)));
+    PK(cudaMemsetAsync(p->cnt_cg.p, 0, sizeof(unsigned) * (B + 1), s));
+    PK(cudaMemsetAsync(p->cgst.p, 0, sizeof(CgState) * B, s));
+    const int nb = cg_matvec_blocks(H, W), nu = cg_update_blocks(p->N);
+    PK(p->part_cg.ensure(sizeof(double) * B * (size_t)(nb > nu ? nb : nu) * 3 + 64));
+  }
+  PK(p->cnt_rec.ensure(sizeof(unsigned) * (B + 1)));
+  PK(cudaMemsetAsync(p->cnt_rec.p, 0, sizeof(unsigned) * (B + 1), s));
   // H^T y / sigma^2 (objective.py:70)
   PK(p->hty.ensure(sizeof(double) * p->N * B));
+  if (!p->fourier) {
+    RUN(ctx, "upsample_corr", launch_upsample_corr(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                                   op->factor, p->htaps.as<double>(), op->ksize,
+                                                   1.0 / (sigma * sigma), s));
+  } else
   RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W, p->htaps.as<double>(),
               op->ksize, 1, 1.0 / (sigma * sigma), s));
   PK(cudaGetLastError());
@@ -593,12 +766,28 @@ void redve_problem_destroy(redve_problem* p) { delete p; }
 
 int redve_fp_step(redve_problem* p, const double* x, double* out, const double* f_ext) {
   redve_ctx* ctx = p->ctx;
-  if (p->dn_kind == DN_EXTERNAL && !f_ext)
-    return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
+  const bool host_dn = p->dn_api_kind == REDVE_DN_EXTERNAL;
+  if (host_dn && !f_ext) return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
   RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream));
+  if (!p->fourier) {
+    int r = fp_step_cg(p, plain(x, p->N), plain(out, p->N), PH_SETUP, host_dn ? f_ext : nullptr);
+    if (r) return r;
+    std::vector<ImgState> hs(p->B);
+    CK(cudaMemcpyAsync(hs.data(), p->state.p, sizeof(ImgState) * p->B, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < p->B; ++b)
+      if (hs[b].err == ERR_CG) return fail(ctx, REDVE_E_CG, "CG residual above 1e-4 ||rhs|| after 200 iterations");
+    return REDVE_OK;
+  }
   DenoiseArgs dn = dn_args(p);
   View xin = plain(x, p->N);
-  if (p->dn_kind == DN_EXTERNAL) {
+  if (p->dn_kind == DN_EXTERNAL) {  // host plug-in or PatchWeighted: f precomputed
+    if (!host_dn) {
+      int r = denoise_to_fbuf(p, plain(x, p->N), PH_SETUP);
+      if (r) return r;
+      f_ext = p->fbuf.as<double>();
+    }
     dn.kind = DN_IDENTITY;
     dn.radius = 0;
     xin = plain(f_ext, p->N);
@@ -633,8 +822,14 @@ static CostArgs cost_args(redve_problem* p, View x, const double* f_ext, int mod
 int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* cost,
                double* fid, double* reg, double* psnr) {
   redve_ctx* ctx = p->ctx;
-  if (p->dn_kind == DN_EXTERNAL && !f_ext)
+  if (p->dn_api_kind == REDVE_DN_EXTERNAL && !f_ext)
     return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
+  if (p->dn_api_kind == REDVE_DN_PATCH) {
+    RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream));
+    int r = denoise_to_fbuf(p, plain(x, p->N), PH_SETUP);
+    if (r) return r;
+    f_ext = p->fbuf.as<double>();
+  }
   StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
   TraceBufs tr;
   memset(&tr, 0, sizeof(tr));
@@ -678,9 +873,9 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   const bool ve = cfg->method == REDVE_METHOD_FP_VE;
   if (ve && cfg->max_inner_steps < cfg->m + cfg->kappa + 2)
     return fail(ctx, REDVE_E_VALUE, "budget must admit at least one full cycle (m + kappa + 2)");
-  if (p->dn_kind == DN_EXTERNAL)
+  if (p->dn_api_kind == REDVE_DN_EXTERNAL)
     return fail(ctx, REDVE_E_UNSUPPORTED, "device solve needs a device denoiser");
-  if (!p->fourier) return fail(ctx, REDVE_E_UNSUPPORTED, "CG path not built yet");
+  const bool pw = p->dn_api_kind == REDVE_DN_PATCH;
 
   const int B = p->B;
   const long long N = p->N;
@@ -753,10 +948,23 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
   va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
 
-  if (track) {  // note_initial (solvers.py:219-223)
-    CostArgs ca = cost_args(p, cur, nullptr, COST_INIT, ctl, tr);
+  // cost evaluation of the current iterates: PatchWeighted needs f(x) first
+  auto cost_of_cur = [&](int mode, StepCtl c) -> int {
+    const double* fe = nullptr;
+    if (pw) {
+      int r = denoise_to_fbuf(p, cur, mode == COST_RECORD ? c.phase : PH_SETUP);
+      if (r) return r;
+      fe = p->fbuf.as<double>();
+    }
+    CostArgs ca = cost_args(p, cur, fe, mode, c, tr);
     RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
     CKL();
+    return REDVE_OK;
+  };
+
+  if (track) {  // note_initial (solvers.py:219-223)
+    int r0 = cost_of_cur(COST_INIT, ctl);
+    if (r0) return r0;
     RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
     CKL();
   }
@@ -765,13 +973,31 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     StepCtl c = ctl;
     c.phase = phase;
     c.defer_commit = cadence ? 1 : 0;
-    int r = fourier_pipeline(p, cur, dn, p->alpha, nxt, p->xb.as<double>(), 1, cur, c, tr, S,
-                             phase);
+    int r;
+    if (p->fourier) {
+      View xin = cur;
+      DenoiseArgs d = dn;
+      if (pw) {
+        r = denoise_to_fbuf(p, cur, phase);
+        if (r) return r;
+        xin = plain(p->fbuf.as<double>(), N);
+        d.kind = DN_IDENTITY;
+        d.radius = 0;
+      }
+      r = fourier_pipeline(p, xin, d, p->alpha, nxt, p->xb.as<double>(), 1, cur, c, tr, S, phase);
+    } else {
+      r = fp_step_cg(p, cur, nxt, phase, nullptr);
+      if (r) return r;
+      RecordArgs ra;
+      ra.N = N; ra.xnew = nxt; ra.xprev = cur; ra.S = S; ra.st = st; ra.ctl = c; ra.tr = tr;
+      ra.partials = p->part_cg.as<double>(); ra.counters = p->cnt_rec.as<unsigned>();
+      RUN(ctx, "step_record", launch_step_record(ra, B, s));
+      CKL();
+    }
     if (r) return r;
     if (cadence) {
-      CostArgs ca = cost_args(p, cur, nullptr, COST_RECORD, c, tr);
-      RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
-      CKL();
+      r = cost_of_cur(COST_RECORD, c);
+      if (r) return r;
       if (track) {
         RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
         CKL();
@@ -788,7 +1014,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     for (int b = 0; b < B; ++b) any |= (hst[b].term == RUNNING);
     return any ? 1 : 0;
   };
-  const int check_every = cfg->tol > 0 ? 1 : 8;
+  const int check_every = (cfg->tol > 0 || !p->fourier) ? 1 : 8;  // CG steps stop exactly
 
   int k = 0;
   if (!ve) {
@@ -834,9 +1060,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     if (r) return r;
   }
   if (track) {  // finalize (solvers.py:255-262)
-    CostArgs ca = cost_args(p, cur, nullptr, COST_FINAL, ctl, tr);
-    RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
-    CKL();
+    int r = cost_of_cur(COST_FINAL, ctl);
+    if (r) return r;
   }
   RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s));
   CKL();

@@ -1,0 +1,472 @@
+// Super-resolution path: PatchWeighted denoiser, fused BlurDownsample normal
+// operator, scipy-exact conjugate gradients, generic step record (fp64).
+//
+// PatchWeighted (denoisers.py:49-129) with its balancing factorised: after
+// t sweeps every map is w_o(p) = w0_o(p) D(p) D(p+o), D = prod of the sweep
+// scalings, so a sweep only updates the scalar field
+//     D(p) <- D(p) / sqrt( D(p) * sum_o w0_o(p) D(p+o) )
+// and f(p) = D(p) sum_o w0_o(p) D(p+o) x(p+o).  Raw weights are symmetric,
+// w0_{-o}(p) = w0_o(p-o), so only the 24 offsets of a half plane are stored.
+//
+// CG (scipy 1.18.1 sparse/linalg/_isolve/iterative.py:311-430 as called by
+// objective.py:105-121): warm start x0 = x_k, stop when ||r|| < 1e-6 ||b||
+// tested before every iteration, r updated recursively, maxiter 200, abort
+// if the true residual exceeds 1e-4 ||rhs|| after maxiter.
+#include "kernels.cuh"
+#include "sr.cuh"
+
+namespace redve {
+
+extern __shared__ __align__(16) unsigned char s_smem[];
+
+static inline int cdivs(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// --------------------------------------------------------------- PatchWeighted
+constexpr int PW_T = 32;  // output tile edge
+
+__device__ __forceinline__ void pw_offset(int k, int sr, int& di, int& dj) {
+  // k-th offset of the half plane {di > 0} U {di == 0, dj > 0}, raster order
+  const int side = 2 * sr + 1;
+  const int lin = (side * side + 1) / 2 + k;  // skip the centre and the negative half
+  di = lin / side - sr;
+  dj = lin % side - sr;
+}
+
+// w0_o(p) = exp(-max(box_{(2pr+1)^2} mean of (x(q)-x(q+o))^2, 0) / h^2)
+__global__ void __launch_bounds__(256) k_pw_weights(PwArgs a) {
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W, pr = a.pr, sr = a.sr;
+  const int halo = pr + sr;
+  const int X = PW_T + 2 * halo;   // x tile edge
+  const int E = PW_T + 2 * pr;     // squared-difference tile edge
+  double* xs = reinterpret_cast<double*>(s_smem);
+  double* es = xs + X * X;
+  double* rs = es + E * E;
+  const int i0 = blockIdx.y * PW_T, j0 = blockIdx.x * PW_T;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    xs[idx] = __ldg(x + (long long)wrap(i0 - halo + ti, H) * W + wrap(j0 - halo + tj, W));
+  }
+  __syncthreads();
+  const long long N = (long long)H * W;
+  const double inv_box = 1.0 / ((2 * pr + 1) * (2 * pr + 1));
+  for (int k = 0; k < a.npos; ++k) {
+    int di, dj;
+    pw_offset(k, sr, di, dj);
+    for (int idx = threadIdx.x; idx < E * E; idx += blockDim.x) {
+      const int ei = idx / E, ej = idx - ei * E;
+      const int ti = ei + sr, tj = ej + sr;  // tile coords of q
+      const double d = xs[ti * X + tj] - xs[(ti + di) * X + tj + dj];
+      es[idx] = d * d;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < E * PW_T; idx += blockDim.x) {
+      const int ei = idx / PW_T, oj = idx - ei * PW_T;
+      double s = 0.0;
+      for (int t = 0; t < 2 * pr + 1; ++t) s += es[ei * E + oj + t];
+      rs[idx] = s;
+    }
+    __syncthreads();
+    double* w0 = a.w0 + ((long long)b * a.npos + k) * N;
+    for (int idx = threadIdx.x; idx < PW_T * PW_T; idx += blockDim.x) {
+      const int oi = idx / PW_T, oj = idx - oi * PW_T;
+      const int gi = i0 + oi, gj = j0 + oj;
+      if (gi >= H || gj >= W) continue;
+      double s = 0.0;
+      for (int t = 0; t < 2 * pr + 1; ++t) s += rs[(oi + t) * PW_T + oj];
+      const double d2 = s * inv_box;
+      w0[(long long)gi * W + gj] = exp(-fmax(d2, 0.0) * a.inv_h2);
+    }
+    __syncthreads();
+  }
+}
+
+// One balancing sweep (apply = 0) or the final application (apply = 1):
+//   S(p) = v(p) + sum_{o in half plane} [ w0_o(p) v(p+o) + w0_o(p-o) v(p-o) ]
+// with v = D (sweep) or v = D x (apply); D_new = D / sqrt(D S), f = D S.
+__global__ void __launch_bounds__(256) k_pw_sweep(PwArgs a, const double* Din, double* Dout,
+                                                  int first, int apply) {
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W, sr = a.sr;
+  const int X = PW_T + 2 * sr;
+  double* vs = reinterpret_cast<double*>(s_smem);
+  const int i0 = blockIdx.y * PW_T, j0 = blockIdx.x * PW_T;
+  const long long N = (long long)H * W;
+  const double* Db = Din + (long long)b * N;
+  const double* x = apply ? a.xin.at(b, a.st) : nullptr;
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    const long long o = (long long)wrap(i0 - sr + ti, H) * W + wrap(j0 - sr + tj, W);
+    const double d = first ? 1.0 : __ldg(Db + o);
+    vs[idx] = apply ? d * __ldg(x + o) : d;
+  }
+  __syncthreads();
+  const double* w0b = a.w0 + (long long)b * a.npos * N;
+  for (int idx = threadIdx.x; idx < PW_T * PW_T; idx += blockDim.x) {
+    const int oi = idx / PW_T, oj = idx - oi * PW_T;
+    const int gi = i0 + oi, gj = j0 + oj;
+    if (gi >= H || gj >= W) continue;
+    const int ci = oi + sr, cj = oj + sr;
+    double S = vs[ci * X + cj];
+    for (int k = 0; k < a.npos; ++k) {
+      int di, dj;
+      pw_offset(k, sr, di, dj);
+      const double* w0 = w0b + (long long)k * N;
+      const double wp = __ldg(w0 + (long long)gi * W + gj);
+      const double wm = __ldg(w0 + (long long)wrap(gi - di, H) * W + wrap(gj - dj, W));
+      S = fma(wp, vs[(ci + di) * X + cj + dj], S);
+      S = fma(wm, vs[(ci - di) * X + cj - dj], S);
+    }
+    const long long o = (long long)gi * W + gj;
+    const double d = first ? 1.0 : Db[o];
+    if (apply) {
+      a.out[(long long)b * N + o] = d * S;
+    } else {
+      Dout[(long long)b * N + o] = d / sqrt(d * S);
+    }
+  }
+}
+
+// Balanced maps of every offset, raster order (denoisers.py:83-111):
+// maps[k](p) = w0_o(p) D(p) D(p+o), w0_{-o}(p) = w0_o(p-o), w0_0 = 1.
+__global__ void k_pw_maps(PwArgs a, const double* D, double* maps) {
+  const int b = blockIdx.y;
+  const int H = a.H, W = a.W, sr = a.sr, side = 2 * sr + 1;
+  const long long N = (long long)H * W;
+  const double* Db = D + (long long)b * N;
+  const double* w0b = a.w0 + (long long)b * a.npos * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+    for (int lin = 0; lin < side * side; ++lin) {
+      const int di = lin / side - sr, dj = lin % side - sr;
+      const int center = (side * side - 1) / 2;
+      double w;
+      if (lin == center) {
+        w = 1.0;
+      } else if (lin > center) {
+        w = w0b[(long long)(lin - center - 1) * N + idx];
+      } else {  // negative offset: mirror plane, evaluated at p + o
+        const int k = (side * side - 1 - lin) - center - 1;
+        w = w0b[(long long)k * N + (long long)wrap(i + di, H) * W + wrap(j + dj, W)];
+      }
+      const double dq = Db[(long long)wrap(i + di, H) * W + wrap(j + dj, W)];
+      maps[((long long)b * side * side + lin) * N + idx] = w * Db[idx] * dq;
+    }
+  }
+}
+
+void launch_pw_maps(const PwArgs& a, cudaStream_t s, int* launches, double* maps) {
+  dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
+  k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
+  const size_t sm = sizeof(double) * (PW_T + 2 * a.sr) * (PW_T + 2 * a.sr);
+  const double* din = a.D0;
+  double* dout = a.D1;
+  for (int it = 0; it < a.iters; ++it) {
+    k_pw_sweep<<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    din = dout;
+    dout = (dout == a.D1) ? a.D0 : a.D1;
+  }
+  k_pw_maps<<<dim3(cdivs((long long)a.H * a.W, 256), a.B), 256, 0, s>>>(a, din, maps);
+  *launches += a.iters + 2;
+}
+
+size_t pw_weights_smem(int pr, int sr) {
+  const int X = PW_T + 2 * (pr + sr), E = PW_T + 2 * pr;
+  return sizeof(double) * ((size_t)X * X + (size_t)E * E + (size_t)E * PW_T);
+}
+
+void launch_pw(const PwArgs& a, cudaStream_t s, int* launches) {
+  dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
+  k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
+  ++*launches;
+  const size_t sm = sizeof(double) * (PW_T + 2 * a.sr) * (PW_T + 2 * a.sr);
+  const double* din = a.D0;
+  double* dout = a.D1;
+  for (int it = 0; it < a.iters; ++it) {
+    k_pw_sweep<<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    ++*launches;
+    din = dout;
+    dout = (dout == a.D1) ? a.D0 : a.D1;
+  }
+  k_pw_sweep<<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+  ++*launches;
+}
+
+// --------------------------------------------------------------- normal operator
+// (A w)(u,v) = (1/sigma^2) (H^T H w)(u,v) + alpha w(u,v),  H = keep(== 0 mod s) o conv.
+// Tile: TH x TW outputs, w tile with halo 2r, zero-filled LR samples z_up with
+// halo r, both in shared memory.
+constexpr int MV_TH = 16, MV_TW = 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
+  const int b = blockIdx.z;
+  CgState& cs = a.cg[b];
+  if (MODE == CG_INIT) {
+    if (!takes_step(a.st[b], a.phase)) return;
+  } else if (MODE == CG_ITER) {
+    if (!cs.active) return;
+  } else {  // CG_RESID
+    if (!takes_step(a.st[b], a.phase) || !cs.need_resid) return;
+  }
+  const int H = a.H, W = a.W, s = a.factor, k = a.k, r = k / 2;
+  const int WX = MV_TW + 4 * r, HX = MV_TH + 4 * r;  // w tile
+  const int WZ = MV_TW + 2 * r, HZ = MV_TH + 2 * r;  // z_up tile
+  double* taps = reinterpret_cast<double*>(s_smem);
+  double* ws = taps + k * k;
+  double* zs = ws + HX * WX;
+  double* red = zs + HZ * WZ;
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x) taps[i] = a.taps[i];
+  const long long N = (long long)H * W;
+  const int i0 = blockIdx.y * MV_TH, j0 = blockIdx.x * MV_TW;
+  const double beta = (MODE == CG_ITER && a.it > 0) ? cs.beta : 0.0;
+  const double* rr = a.r + (long long)b * N;
+  const double* pold = a.p + (long long)b * N;
+  const double* xin = (MODE == CG_ITER) ? nullptr : a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < HX * WX; idx += blockDim.x) {
+    const int ti = idx / WX, tj = idx - ti * WX;
+    const long long o = (long long)wrap(i0 - 2 * r + ti, H) * W + wrap(j0 - 2 * r + tj, W);
+    double w;
+    if (MODE == CG_ITER) w = (a.it > 0) ? fma(beta, pold[o], rr[o]) : rr[o];
+    else w = xin[o];
+    ws[idx] = w;
+  }
+  __syncthreads();
+  // z_up(u, v) = (H w)(u, v) at measurement-grid points, 0 elsewhere
+  for (int idx = threadIdx.x; idx < HZ * WZ; idx += blockDim.x) {
+    const int zi = idx / WZ, zj = idx - zi * WZ;
+    const int gu = wrap(i0 - r + zi, H), gv = wrap(j0 - r + zj, W);
+    double z = 0.0;
+    if ((gu % s) == 0 && (gv % s) == 0) {
+      for (int ta = 0; ta < k; ++ta)
+        for (int tb = 0; tb < k; ++tb)
+          z = fma(taps[ta * k + tb], ws[(zi + r - (ta - r)) * WX + (zj + r - (tb - r))], z);
+    }
+    zs[idx] = z;
+  }
+  __syncthreads();
+  double acc[2] = {0.0, 0.0};
+  const double inv_s2 = a.inv_sigma2;
+  for (int idx = threadIdx.x; idx < MV_TH * MV_TW; idx += blockDim.x) {
+    const int oi = idx / MV_TW, oj = idx - oi * MV_TW;
+    const int gi = i0 + oi, gj = j0 + oj;
+    if (gi >= H || gj >= W) continue;
+    double ht = 0.0;  // (H^T z_up)(u, v): correlation
+    for (int ta = 0; ta < k; ++ta)
+      for (int tb = 0; tb < k; ++tb)
+        ht = fma(taps[ta * k + tb], zs[(oi + r + (ta - r)) * WZ + (oj + r + (tb - r))], ht);
+    const double wv = ws[(oi + 2 * r) * WX + (oj + 2 * r)];
+    const double aw = fma(ht, inv_s2, a.alpha * wv);
+    const long long o = (long long)b * N + (long long)gi * W + gj;
+    if (MODE == CG_ITER) {
+      a.p[o] = wv;
+      a.q[o] = aw;
+      acc[0] = fma(wv, aw, acc[0]);
+    } else {
+      const double bb = fma(a.alpha, a.f[o], a.hty[o]);  // rhs = H^T y/sigma^2 + alpha f
+      const double res = bb - aw;
+      if (MODE == CG_INIT) {
+        a.r[o] = res;
+        a.xout.at(b, a.st)[(long long)gi * W + gj] = wv;  // warm start copy x <- x_k
+      }
+      acc[0] = fma(bb, bb, acc[0]);
+      acc[1] = fma(res, res, acc[1]);
+    }
+  }
+  block_sum<2>(acc, red);
+  const int nblk = gridDim.x * gridDim.y;
+  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) {
+    a.partials[((long long)b * nblk + blk) * 2] = acc[0];
+    a.partials[((long long)b * nblk + blk) * 2 + 1] = acc[1];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = 0; i < nblk; ++i) {
+      t0 += ((volatile double*)a.partials)[((long long)b * nblk + i) * 2];
+      t1 += ((volatile double*)a.partials)[((long long)b * nblk + i) * 2 + 1];
+    }
+    if (MODE == CG_ITER) {
+      cs.alpha = cs.rho / t0;  // rho_cur / (p . q)
+    } else if (MODE == CG_INIT) {
+      const double bn = sqrt(t0);
+      cs.bn2 = t0;
+      cs.atol = a.rtol * bn;  // max(atol=0, rtol*||b||)
+      cs.rho = t1;
+      cs.its = 0;
+      cs.info = 0;
+      cs.need_resid = 0;
+      cs.zero_b = (bn == 0.0);
+      cs.active = !(cs.zero_b || sqrt(t1) < cs.atol);
+    } else {  // residual check after maxiter (objective.py:114-120)
+      if (sqrt(t1) > a.abort * sqrt(t0)) a.st[b].err = ERR_CG;
+      cs.need_resid = 0;
+    }
+  }
+}
+
+// x += alpha p ; r -= alpha q ; rho = r.r ; stopping decisions
+__global__ void __launch_bounds__(256) k_cg_update(CgArgs a) {
+  const int b = blockIdx.y;
+  CgState& cs = a.cg[b];
+  if (!cs.active) return;
+  const long long N = (long long)a.H * a.W;
+  const double al = cs.alpha;
+  double* x = a.xout.at(b, a.st);
+  double* r = a.r + (long long)b * N;
+  const double* p = a.p + (long long)b * N;
+  const double* q = a.q + (long long)b * N;
+  double acc[1] = {0.0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = fma(al, p[i], x[i]);
+    const double rn = fma(-al, q[i], r[i]);
+    r[i] = rn;
+    acc[0] = fma(rn, rn, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0) a.partials[(long long)b * nblk + blockIdx.x] = acc[0];
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double rho = 0.0;
+    for (int i = 0; i < nblk; ++i) rho += ((volatile double*)a.partials)[(long long)b * nblk + i];
+    const double rho_prev = cs.rho;
+    cs.its += 1;
+    if (cs.its >= a.maxiter) {  // loop exhausted: info = maxiter, no final test
+      cs.active = 0;
+      cs.info = a.maxiter;
+      cs.need_resid = 1;
+    } else if (sqrt(rho) < cs.atol) {
+      cs.active = 0;
+    }
+    cs.beta = rho / rho_prev;
+    cs.rho = rho;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st[b].cg_its = cs.its;
+}
+
+// ||b|| == 0: scipy returns b itself (the zero vector)
+__global__ void k_cg_zero_b(CgArgs a) {
+  const int b = blockIdx.y;
+  if (!takes_step(a.st[b], a.phase) || !a.cg[b].zero_b) return;
+  const long long N = (long long)a.H * a.W;
+  double* x = a.xout.at(b, a.st);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = 0.0;
+}
+
+size_t cg_matvec_smem(int k) {
+  const int r = k / 2;
+  return sizeof(double) * ((size_t)k * k + (size_t)(MV_TH + 4 * r) * (MV_TW + 4 * r) +
+                           (size_t)(MV_TH + 2 * r) * (MV_TW + 2 * r) + 64);
+}
+
+template <int MODE>
+static void matvec_t(const CgArgs& a, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_cg_matvec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    done = true;
+  }
+  dim3 grid(cdivs(a.W, MV_TW), cdivs(a.H, MV_TH), a.B);
+  k_cg_matvec<MODE><<<grid, 256, cg_matvec_smem(a.k), s>>>(a);
+}
+
+int cg_matvec_blocks(int H, int W) { return cdivs(W, MV_TW) * cdivs(H, MV_TH); }
+int cg_update_blocks(long long N) {
+  int c = cdivs(N, 256 * 8);
+  return c > 256 ? 256 : (c < 1 ? 1 : c);
+}
+
+void launch_cg_init(const CgArgs& a, cudaStream_t s) { matvec_t<CG_INIT>(a, s); }
+void launch_cg_iter(const CgArgs& a, cudaStream_t s) { matvec_t<CG_ITER>(a, s); }
+void launch_cg_resid(const CgArgs& a, cudaStream_t s) { matvec_t<CG_RESID>(a, s); }
+void launch_cg_update(const CgArgs& a, cudaStream_t s) {
+  k_cg_update<<<dim3(cg_update_blocks((long long)a.H * a.W), a.B), 256, 0, s>>>(a);
+}
+void launch_cg_zero_b(const CgArgs& a, cudaStream_t s) {
+  k_cg_zero_b<<<dim3(cg_update_blocks((long long)a.H * a.W), a.B), 256, 0, s>>>(a);
+}
+
+// --------------------------------------------------------------- stencil denoisers into f
+// f(x) for the CG route (the Fourier route fuses them into k_row_fwd).
+__global__ void __launch_bounds__(256) k_denoise_view(View xin, DenoiseArgs dn, double* out,
+                                                      const ImgState* st, int phase, int H, int W) {
+  const int b = blockIdx.y;
+  if (!takes_step(st[b], phase)) return;
+  const long long N = (long long)H * W;
+  const double* x = xin.at(b, st);
+  double* o = out + (long long)b * N;
+  const int r = dn.ksize / 2;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+    double v;
+    if (dn.kind == DN_MEDIAN3) {
+      double q[9];
+      int n = 0;
+      for (int a = -1; a <= 1; ++a)
+        for (int c = -1; c <= 1; ++c) q[n++] = __ldg(x + (long long)wrap(i + a, H) * W + wrap(j + c, W));
+      v = median9(q);
+    } else if (dn.kind == DN_CONV) {
+      v = 0.0;
+      for (int a = 0; a < dn.ksize; ++a)
+        for (int c = 0; c < dn.ksize; ++c)
+          v = fma(dn.taps[a * dn.ksize + c],
+                  __ldg(x + (long long)wrap(i - (a - r), H) * W + wrap(j - (c - r), W)), v);
+    } else {
+      v = x[idx];
+    }
+    o[idx] = v;
+  }
+}
+
+void launch_denoise_view(View xin, DenoiseArgs dn, double* out, const ImgState* st, int phase,
+                         int B, int H, int W, cudaStream_t s) {
+  k_denoise_view<<<dim3(cg_update_blocks((long long)H * W), B), 256, 0, s>>>(xin, dn, out, st,
+                                                                           phase, H, W);
+}
+
+// --------------------------------------------------------------- step record
+// ||x+ - x||, ||x||, finiteness -> record_step (solvers.py:225-253)
+__global__ void __launch_bounds__(256) k_step_record(RecordArgs a) {
+  const int b = blockIdx.y;
+  if (!takes_step(a.st[b], a.ctl.phase)) return;
+  const double* xn = a.xnew.at(b, a.st);
+  const double* xp = a.xprev.at(b, a.st);
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.N;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = xn[i], u = xp[i], d = v - u;
+    acc[0] = fma(d, d, acc[0]);
+    acc[1] = fma(u, u, acc[1]);
+    acc[2] += isfinite(v) ? 0.0 : 1.0;
+  }
+  __shared__ double red[96];
+  block_sum<3>(acc, red);
+  const int nblk = gridDim.x;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 3; ++i) a.partials[((long long)b * nblk + blockIdx.x) * 3 + i] = acc[i];
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double t[3] = {0, 0, 0};
+    for (int i = 0; i < nblk; ++i)
+      for (int j = 0; j < 3; ++j) t[j] += ((volatile double*)a.partials)[((long long)b * nblk + i) * 3 + j];
+    record_step(a.st[b], b, t[0], t[1], t[2], a.S, a.ctl, a.tr);
+  }
+}
+
+void launch_step_record(const RecordArgs& a, int B, cudaStream_t s) {
+  k_step_record<<<dim3(cg_update_blocks(a.N), B), 256, 0, s>>>(a);
+}
+
+}  // namespace redve

@@ -17,7 +17,7 @@ from . import _io
 from . import _native as nat
 from .imaging import Psf, make_psf
 
-__all__ = ["Identity", "GaussianFilter", "Median3", "NotLinear", "materialize_dense",
+__all__ = ["Identity", "GaussianFilter", "Median3", "PatchWeighted", "NotLinear", "materialize_dense",
            "BUILTIN_DENOISERS", "denoise"]
 
 
@@ -86,6 +86,64 @@ class Median3(_Native):
     linear = False
 
 
+class PatchWeighted(_Native):
+    """Symmetric non-local-means smoother (denoisers.py:49-129).
+
+    Same parameters and results as the reference; on the device the 20
+    balancing sweeps update one scalar field D (w_o(p) = w0_o(p) D(p) D(p+o))
+    instead of 49 maps, and only the 24 half-plane raw-weight maps are stored."""
+
+    kind = nat.DN_PATCH
+    linear = False
+
+    def __init__(self, patch_radius: int = 1, search_radius: int = 3, h: float = 110.0,
+                 balance_iters: int = 20):
+        if patch_radius < 0 or search_radius < 1 or h <= 0 or balance_iters < 1:
+            raise ValueError("need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1")
+        self.patch_radius = int(patch_radius)
+        self.search_radius = int(search_radius)
+        self.h = float(h)
+        self.balance_iters = int(balance_iters)
+        self.name = f"patch_weighted(p={patch_radius},s={search_radius},h={h:g})"
+
+    def _fill(self, d):
+        d.patch_radius = self.patch_radius
+        d.search_radius = self.search_radius
+        d.balance_iters = self.balance_iters
+        d.h = self.h
+
+    def weight_maps(self, x):
+        """(offsets, maps): the balanced weight of every search offset (denoisers.py:83-111)."""
+        t, from_np = _io.to_device(x)
+        if t.dim() != 2:
+            raise ValueError("weight_maps takes one image")
+        t = t.contiguous()
+        r = self.search_radius
+        side = 2 * r + 1
+        maps = _io.empty((side * side,) + tuple(t.shape))
+        ctx = nat.context()
+        d = self._desc()
+        nat.check(nat.library().redve_patch_weight_maps(ctx, C.byref(d), 1, t.shape[0], t.shape[1],
+                                                        nat.dptr(t), nat.dptr(maps)), ctx)
+        offsets = [(di, dj) for di in range(-r, r + 1) for dj in range(-r, r + 1)]
+        m = _io.to_host(maps, True)
+        return offsets, [m[k] for k in range(side * side)]
+
+    @staticmethod
+    def apply_maps(offsets, maps, z):
+        """Apply a frozen weight field (denoisers.py:113-119)."""
+        z = np.asarray(z, dtype=np.float64)
+        out = np.zeros_like(z)
+        for (di, dj), w in zip(offsets, maps):
+            out += w * np.roll(z, (-di, -dj), axis=(0, 1))
+        return out
+
+    def linearized(self, x):
+        """The denoiser with its weight field frozen at x (denoisers.py:121-124)."""
+        offsets, maps = self.weight_maps(x)
+        return lambda z: self.apply_maps(offsets, maps, np.asarray(z, dtype=np.float64))
+
+
 def denoise(spec, x):
     """denoisers.py:132-134."""
     from .imaging import as_image
@@ -113,5 +171,6 @@ def materialize_dense(spec, width: int, height: int) -> np.ndarray:
 BUILTIN_DENOISERS = {
     "identity": Identity,
     "gaussian": GaussianFilter,
+    "patch-weighted": PatchWeighted,
     "median3": Median3,
 }

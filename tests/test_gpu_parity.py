@@ -257,3 +257,72 @@ class TestSolves:
                                     reference=truths[b].ravel())
             assert rel(X[b].ravel(), xo) <= 1e-5
             np.testing.assert_allclose(traces[b].costs(), tro.as_arrays()["cost"], rtol=1e-9)
+
+
+# --------------------------------------------------------------------- super-resolution
+class TestSuperres:
+    def test_patch_weighted_golden(self, rv, golden):
+        g = golden("operators.npz")
+        n = 0
+        for i in range(6):
+            if f"patch{i}" in g:
+                assert rel(rv.PatchWeighted()(g[f"x{i}"]), g[f"patch{i}"]) <= 1e-12
+                n += 1
+        assert n >= 3
+
+    @pytest.mark.parametrize("shape", [(32, 40), (96, 96), (70, 33)])
+    def test_patch_weighted_vs_oracle(self, rv, R, shape):
+        x = np.random.default_rng(7).uniform(0, 255, shape)
+        assert rel(rv.PatchWeighted()(x), R.patch_weighted(x)) <= 1e-12
+        assert rel(rv.PatchWeighted(2, 2, 60.0, 7)(x), R.patch_weighted(x, 2, 2, 60.0, 7)) <= 1e-12
+
+    def test_weight_maps_vs_oracle(self, rv, R):
+        x = np.random.default_rng(8).uniform(0, 255, (20, 24))
+        offs, maps = rv.PatchWeighted().weight_maps(x)
+        offs_o, maps_o = R.patch_weight_maps(x)
+        assert offs == offs_o
+        for a, b in zip(maps, maps_o):
+            np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-15)
+
+    def test_cg_step_ragged_golden(self, rv, golden):
+        g = golden("superres.npz")
+        truth = g["sr_ragged/truth"]
+        op = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, truth.shape)
+        obj = rv.RedObjective(op, g["sr_ragged/y"], 5.0, 0.02, rv.GaussianFilter())
+        assert rel(obj.fp_step(g["sr_ragged/x"]), g["sr_ragged/step"]) <= 1e-9
+
+    def test_cg_step_patch_golden(self, rv, golden):
+        g = golden("superres.npz")
+        truth, y, x0 = g["sr48/truth"], g["sr48/y"], g["sr48/x0"]
+        op = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, truth.shape)
+        assert rel(op.adjoint(y), x0) <= 1e-13
+        obj = rv.RedObjective(op, y, 5.0, 0.02, rv.PatchWeighted())
+        assert rel(obj.fp_step(x0), g["sr48/step1"]) <= 1e-9
+
+    @pytest.mark.parametrize("name,method,ve_method", [("fp", "fp", "mpe"), ("rre", "fp-ve", "rre")])
+    def test_sr48_solve_vs_reference(self, rv, golden, name, method, ve_method):
+        g = golden("superres.npz")
+        truth, y, x0 = g["sr48/truth"], g["sr48/y"], g["sr48/x0"]
+        op = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, truth.shape)
+        obj = rv.RedObjective(op, y, 5.0, 0.02, rv.PatchWeighted())
+        prob = rv.as_fixed_point_problem(obj, reference=truth)
+        x, tr = rv.solve(prob, x0.ravel(), rv.SolveConfig(method=method, ve_method=ve_method,
+                                                          max_inner_steps=30))
+        assert rel(x, g[f"sr48/{name}/x"]) <= 1e-5
+        _cmp_trace(tr, g, f"sr48/{name}", cost_rtol=1e-8)
+
+    def test_sr_cost_vs_oracle(self, rv, R):
+        rng = np.random.default_rng(3)
+        shape = (36, 30)
+        truth = rng.uniform(0, 255, shape)
+        op_o = R.BlurDecimate(R.psf_taps("gaussian", 7, 1.6), 3, shape)
+        y = R.measure(truth, op_o, 5.0, 2)
+        for den_d, den_o in ((rv.PatchWeighted(), R.patch_weighted), (rv.Median3(), None)):
+            from oracle import extras
+            den_o = den_o or extras.median3
+            obj = rv.RedObjective(rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, shape), y,
+                                  5.0, 0.02, den_d)
+            red = R.Red(op_o, y, 5.0, 0.02, den_o)
+            x = rng.uniform(0, 255, shape)
+            assert abs(obj.cost(x) - red.cost(x)) <= 1e-10 * abs(red.cost(x))
+            assert rel(obj.fp_step(x), red.fp_step(x)) <= 1e-9
