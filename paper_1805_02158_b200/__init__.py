@@ -8,8 +8,8 @@ fallback.  ``RedBatch`` / ``solve_batch`` add the batched device API.
 """
 
 from .batch import RedBatch, solve_batch
-from .denoisers import (BUILTIN_DENOISERS, GaussianFilter, Identity, Median3, NotLinear,
-                        PatchWeighted, denoise, materialize_dense)
+from .denoisers import (BUILTIN_DENOISERS, FilterBank, GaussianFilter, Identity, Median3,
+                        NotLinear, PatchWeighted, denoise, materialize_dense)
 from .errors import (CgNoConvergence, DegenerateSum, InvalidSize, KernelTooLarge, NoConvergence,
                      NonFiniteIterate, RankDeficient, ShapeMismatch, ZeroFirstColumn)
 from .extrapolation import (METHODS, MPE, RRE, SVDMPE, ExtrapolationResult, ExtrapolationWeights,

@@ -13,6 +13,7 @@
 
 #include "../../include/redve_b200.h"
 #include "kernels.cuh"
+#include "rd.cuh"
 #include "sr.cuh"
 
 using namespace redve;
@@ -214,6 +215,9 @@ struct redve_problem {
   int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
   double pw_h = 110.0;
   DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
+  int rd_nf = 0, rd_fs = 0;
+  double rd_tau = 0.0;
+  DevBuf rd_filters, rd_scales;
   DevBuf htaps, dntaps, y, ref, hty, xb, g, Z, state, partials, cnt_inv, cnt_cost, cnt_ve,
       fbuf, ring, best, q, trace, vals;
   bool has_ref = false;
@@ -293,7 +297,13 @@ static View plain(const double* base, long long N) {
 // (PatchWeighted always; the stencils on the CG route).
 static int denoise_to_fbuf(redve_problem* p, View x, int phase) {
   redve_ctx* ctx = p->ctx;
-  if (p->dn_api_kind == REDVE_DN_PATCH) {
+  if (p->dn_api_kind == REDVE_DN_FILTERBANK) {
+    RdArgs a;
+    a.B = p->B; a.H = p->H; a.W = p->W; a.nf = p->rd_nf; a.fs = p->rd_fs;
+    a.filters = p->rd_filters.as<double>(); a.scales = p->rd_scales.as<double>(); a.tau = p->rd_tau;
+    a.xin = x; a.out = p->fbuf.as<double>(); a.st = p->state.as<ImgState>(); a.phase = phase;
+    RUN(ctx, "filter_bank", launch_rd(a, ctx->stream));
+  } else if (p->dn_api_kind == REDVE_DN_PATCH) {
     PwArgs a;
     a.B = p->B; a.H = p->H; a.W = p->W;
     a.pr = p->pw_pr; a.sr = p->pw_sr; a.npos = p->pw_npos; a.iters = p->pw_iters;
@@ -468,6 +478,26 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       CK(cudaStreamSynchronize(ctx->stream));
       return REDVE_OK;
     }
+    case REDVE_DN_FILTERBANK: {
+      if (dn->n_filters < 1 || !is_odd_pos(dn->fsize) || dn->fsize > 15)
+        return fail(ctx, REDVE_E_VALUE, "filter bank needs n_filters >= 1 and an odd size <= 15");
+      const size_t fb = sizeof(double) * dn->n_filters * dn->fsize * dn->fsize;
+      CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
+      CK(ctx->scratch_a.ensure(fb + sizeof(double) * dn->n_filters));
+      CK(cudaMemcpyAsync(ctx->scratch_a.p, dn->filters, fb, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->scratch_a.as<char>() + fb, dn->scales,
+                         sizeof(double) * dn->n_filters, cudaMemcpyHostToDevice, ctx->stream));
+      RdArgs a;
+      a.B = B; a.H = H; a.W = W; a.nf = dn->n_filters; a.fs = dn->fsize;
+      a.filters = ctx->scratch_a.as<double>();
+      a.scales = reinterpret_cast<const double*>(ctx->scratch_a.as<char>() + fb);
+      a.tau = dn->tau; a.xin = plain(x, N); a.out = out;
+      a.st = ctx->ve_state.as<ImgState>(); a.phase = PH_SETUP;
+      RUN(ctx, "filter_bank", launch_rd(a, ctx->stream));
+      CKL();
+      CK(cudaStreamSynchronize(ctx->stream));
+      return REDVE_OK;
+    }
     case REDVE_DN_PATCH: {
       if (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1)
         return fail(ctx, REDVE_E_VALUE,
@@ -596,13 +626,17 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
       return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
   }
   if (dn->kind != REDVE_DN_IDENTITY && dn->kind != REDVE_DN_CONV && dn->kind != REDVE_DN_MEDIAN3 &&
-      dn->kind != REDVE_DN_EXTERNAL && dn->kind != REDVE_DN_PATCH)
+      dn->kind != REDVE_DN_EXTERNAL && dn->kind != REDVE_DN_PATCH &&
+      dn->kind != REDVE_DN_FILTERBANK)
     return fail(ctx, REDVE_E_UNSUPPORTED, "denoiser kind %d not available in this build",
                 dn->kind);
   if (dn->kind == REDVE_DN_PATCH &&
       (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1))
     return fail(ctx, REDVE_E_VALUE,
                 "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+  if (dn->kind == REDVE_DN_FILTERBANK &&
+      (dn->n_filters < 1 || !is_odd_pos(dn->fsize) || dn->fsize > 15 || !dn->filters || !dn->scales))
+    return fail(ctx, REDVE_E_VALUE, "filter bank needs n_filters >= 1 and an odd size <= 15");
   if (op->kind == REDVE_OP_BLUR) {  // Fourier route limits
     if (H > 4096 || W > 4096) return fail(ctx, REDVE_E_UNSUPPORTED, "image side > 4096");
     if (!is_pow2(H) && H > 256) return fail(ctx, REDVE_E_UNSUPPORTED, "non power-of-two side > 256");
@@ -703,6 +737,18 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   PK(cudaMemsetAsync(p->cnt_cost.p, 0, sizeof(unsigned) * (B + 1), s));
   PK(cudaMemsetAsync(p->cnt_ve.p, 0, sizeof(unsigned) * (B + 1), s));
   PK(p->vals.ensure(sizeof(double) * 3 * B));
+  if (dn->kind == REDVE_DN_FILTERBANK) {
+    p->rd_nf = dn->n_filters;
+    p->rd_fs = dn->fsize;
+    p->rd_tau = dn->tau;
+    const size_t fb = sizeof(double) * dn->n_filters * dn->fsize * dn->fsize;
+    PK(p->rd_filters.ensure(fb));
+    PK(cudaMemcpyAsync(p->rd_filters.p, dn->filters, fb, cudaMemcpyHostToDevice, s));
+    PK(p->rd_scales.ensure(sizeof(double) * dn->n_filters));
+    PK(cudaMemcpyAsync(p->rd_scales.p, dn->scales, sizeof(double) * dn->n_filters,
+                       cudaMemcpyHostToDevice, s));
+    PK(cudaStreamSynchronize(s));  // host parameter arrays may go away
+  }
   // device denoiser output / PatchWeighted fields
   if (dn->kind != REDVE_DN_EXTERNAL) PK(p->fbuf.ensure(sizeof(double) * p->N * B));
   if (dn->kind == REDVE_DN_PATCH) {
@@ -824,7 +870,7 @@ int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* c
   redve_ctx* ctx = p->ctx;
   if (p->dn_api_kind == REDVE_DN_EXTERNAL && !f_ext)
     return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
-  if (p->dn_api_kind == REDVE_DN_PATCH) {
+  if (p->dn_api_kind == REDVE_DN_PATCH || p->dn_api_kind == REDVE_DN_FILTERBANK) {
     RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), p->B, ctx->stream));
     int r = denoise_to_fbuf(p, plain(x, p->N), PH_SETUP);
     if (r) return r;
@@ -875,7 +921,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     return fail(ctx, REDVE_E_VALUE, "budget must admit at least one full cycle (m + kappa + 2)");
   if (p->dn_api_kind == REDVE_DN_EXTERNAL)
     return fail(ctx, REDVE_E_UNSUPPORTED, "device solve needs a device denoiser");
-  const bool pw = p->dn_api_kind == REDVE_DN_PATCH;
+  const bool pw = p->dn_api_kind == REDVE_DN_PATCH || p->dn_api_kind == REDVE_DN_FILTERBANK;
 
   const int B = p->B;
   const long long N = p->N;

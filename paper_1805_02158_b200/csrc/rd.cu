@@ -1,0 +1,82 @@
+// Seeded reaction-diffusion (filter-bank) denoiser for BASELINE.json configs[3]:
+//   f(x) = x - tau * sum_i  k_i (*) phi_i( k_i (x) x ),   phi_i(z) = z / (1 + z^2 / s_i^2)
+// ((x) = periodic correlation, (*) = its adjoint, the periodic convolution).
+// One fused tiled kernel: x tile with halo 2r, every filter's influence
+// response phi_i on the tile with halo r kept in shared memory, then the
+// adjoint filters back -- x is read once and f written once.
+// No reference implementation exists: the in-repo
+// oracle is oracle/extras.py FilterBank ("parity unpinned").
+#include "kernels.cuh"
+#include "rd.cuh"
+
+namespace redve {
+
+extern __shared__ __align__(16) unsigned char r_smem[];
+
+constexpr int RD_T = 32;
+
+__global__ void __launch_bounds__(256) k_rd_denoise(RdArgs a) {
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W, fs = a.fs, r = fs / 2, nf = a.nf;
+  const int X = RD_T + 4 * r;  // x tile edge
+  const int P = RD_T + 2 * r;  // phi tile edge
+  double* ks = reinterpret_cast<double*>(r_smem);
+  double* sc = ks + nf * fs * fs;
+  double* xs = sc + nf;
+  double* ph = xs + X * X;
+  for (int i = threadIdx.x; i < nf * fs * fs; i += blockDim.x) ks[i] = a.filters[i];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) sc[i] = 1.0 / (a.scales[i] * a.scales[i]);
+  const int i0 = blockIdx.y * RD_T, j0 = blockIdx.x * RD_T;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    xs[idx] = __ldg(x + (long long)wrap(i0 - 2 * r + ti, H) * W + wrap(j0 - 2 * r + tj, W));
+  }
+  __syncthreads();
+  // phi_i over the tile + halo r: z(q) = sum_ab k[a][b] x(q + (a-r, b-r))
+  for (int idx = threadIdx.x; idx < nf * P * P; idx += blockDim.x) {
+    const int f = idx / (P * P), rem = idx - f * P * P;
+    const int pi = rem / P, pj = rem - pi * P;
+    const double* kf = ks + f * fs * fs;
+    double z = 0.0;
+    for (int ta = 0; ta < fs; ++ta)
+      for (int tb = 0; tb < fs; ++tb) z = fma(kf[ta * fs + tb], xs[(pi + ta) * X + (pj + tb)], z);
+    ph[idx] = z / fma(z * z, sc[f], 1.0);
+  }
+  __syncthreads();
+  const long long N = (long long)H * W;
+  for (int idx = threadIdx.x; idx < RD_T * RD_T; idx += blockDim.x) {
+    const int oi = idx / RD_T, oj = idx - oi * RD_T;
+    const int gi = i0 + oi, gj = j0 + oj;
+    if (gi >= H || gj >= W) continue;
+    // adjoint: sum_ab k[a][b] phi(p - (a-r, b-r))
+    double acc = 0.0;
+    for (int f = 0; f < nf; ++f) {
+      const double* kf = ks + f * fs * fs;
+      const double* pf = ph + f * P * P;
+      for (int ta = 0; ta < fs; ++ta)
+        for (int tb = 0; tb < fs; ++tb)
+          acc = fma(kf[ta * fs + tb], pf[(oi + 2 * r - ta) * P + (oj + 2 * r - tb)], acc);
+    }
+    const double xv = xs[(oi + 2 * r) * X + (oj + 2 * r)];
+    a.out[(long long)b * N + (long long)gi * W + gj] = fma(-a.tau, acc, xv);
+  }
+}
+
+size_t rd_smem(int nf, int fs) {
+  const int r = fs / 2, X = RD_T + 4 * r, P = RD_T + 2 * r;
+  return sizeof(double) * ((size_t)nf * fs * fs + nf + (size_t)X * X + (size_t)nf * P * P);
+}
+
+void launch_rd(const RdArgs& a, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_rd_denoise, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+  }
+  dim3 grid((a.W + RD_T - 1) / RD_T, (a.H + RD_T - 1) / RD_T, a.B);
+  k_rd_denoise<<<grid, 256, rd_smem(a.nf, a.fs), s>>>(a);
+}
+
+}  // namespace redve

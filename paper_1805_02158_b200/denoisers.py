@@ -17,7 +17,7 @@ from . import _io
 from . import _native as nat
 from .imaging import Psf, make_psf
 
-__all__ = ["Identity", "GaussianFilter", "Median3", "PatchWeighted", "NotLinear", "materialize_dense",
+__all__ = ["Identity", "GaussianFilter", "Median3", "PatchWeighted", "FilterBank", "NotLinear", "materialize_dense",
            "BUILTIN_DENOISERS", "denoise"]
 
 
@@ -144,6 +144,46 @@ class PatchWeighted(_Native):
         return lambda z: self.apply_maps(offsets, maps, np.asarray(z, dtype=np.float64))
 
 
+def filter_bank_params(seed: int = 0, n_filters: int = 8, size: int = 5):
+    """Seeded filter-bank parameters (BASELINE.json configs[3]: "parameters drawn
+    from the seed"): zero-mean unit-norm k x k filters, influence scales in
+    [10, 40], step tau = 0.5 / sum ||k_i||_1^2, drawn from PCG64(seed) in a fixed
+    order (host-side setup, like the reference's seeded noise)."""
+    gen = np.random.Generator(np.random.PCG64(seed))
+    k = gen.standard_normal((n_filters, size, size))
+    k -= k.mean(axis=(1, 2), keepdims=True)
+    k /= np.sqrt((k**2).sum(axis=(1, 2), keepdims=True))
+    scales = 10.0 + 30.0 * gen.random(n_filters)
+    l1 = np.abs(k).sum(axis=(1, 2))
+    tau = 0.5 / float((l1**2).sum())
+    return np.ascontiguousarray(k), np.ascontiguousarray(scales), tau
+
+
+class FilterBank(_Native):
+    """One reaction-diffusion stage f(x) = x - tau sum_i k_i * phi_i(k_i (x) x),
+    phi_i(z) = z / (1 + z^2/s_i^2) (the "reaction-diffusion filter bank with its
+    influence nonlinearity" of BASELINE.json configs[3]; the reference has no
+    such denoiser -- TNRD is out of its scope).  One fused CUDA
+    stencil kernel per call."""
+
+    kind = nat.DN_FILTERBANK
+    linear = False
+
+    def __init__(self, seed: int = 0, n_filters: int = 8, size: int = 5):
+        if n_filters < 1 or size < 1 or size % 2 == 0:
+            raise ValueError("need n_filters >= 1 and an odd filter size")
+        self.seed, self.n_filters, self.size = int(seed), int(n_filters), int(size)
+        self.k, self.s, self.tau = filter_bank_params(seed, n_filters, size)
+        self.name = f"filter_bank(seed={seed},n={n_filters},k={size})"
+
+    def _fill(self, d):
+        d.n_filters = self.n_filters
+        d.fsize = self.size
+        d.filters = nat.hptr(self.k)
+        d.scales = nat.hptr(self.s)
+        d.tau = self.tau
+
+
 def denoise(spec, x):
     """denoisers.py:132-134."""
     from .imaging import as_image
@@ -173,4 +213,5 @@ BUILTIN_DENOISERS = {
     "gaussian": GaussianFilter,
     "patch-weighted": PatchWeighted,
     "median3": Median3,
+    "filter-bank": FilterBank,
 }

@@ -326,3 +326,33 @@ class TestSuperres:
             x = rng.uniform(0, 255, shape)
             assert abs(obj.cost(x) - red.cost(x)) <= 1e-10 * abs(red.cost(x))
             assert rel(obj.fp_step(x), red.fp_step(x)) <= 1e-9
+
+
+# --------------------------------------------------------------------- filter bank (configs[3])
+class TestFilterBank:
+    @pytest.mark.parametrize("shape", [(32, 32), (64, 48), (100, 70)])
+    def test_vs_oracle(self, rv, shape):
+        from oracle import extras
+
+        x = np.random.default_rng(11).uniform(0, 255, shape)
+        for seed in (0, 3):
+            assert rel(rv.FilterBank(seed)(x), extras.FilterBank(seed)(x)) <= 1e-13
+
+    def test_deblur_solve_vs_oracle(self, rv, R):
+        from oracle import extras
+        from paper_1805_02158_b200.synth import voronoi_scene
+
+        n, B = 64, 3
+        truths = np.stack([voronoi_scene(s + 10, n) for s in range(B)])
+        op_o = R.CirculantBlur(R.psf_taps("uniform", 9), (n, n))
+        ys = np.stack([R.measure(truths[b], op_o, SQRT2, b) for b in range(B)])
+        batch = rv.RedBatch(rv.Blur(rv.make_psf("uniform", 9), (n, n)), ys, SQRT2, 0.02,
+                            rv.FilterBank(0), truths)
+        X, traces = rv.solve_batch(batch, ys, rv.SolveConfig(method="fp-ve", max_inner_steps=24))
+        X = X.cpu().numpy()
+        for b in range(B):
+            step, cost = R.red_problem(R.Red(op_o, ys[b], SQRT2, 0.02, extras.FilterBank(0)))
+            xo, tro = R.run_cycling(step, ys[b], 24, "mpe", objective=cost,
+                                    reference=truths[b].ravel())
+            assert rel(X[b].ravel(), xo) <= 1e-5
+            np.testing.assert_allclose(traces[b].costs(), tro.as_arrays()["cost"], rtol=1e-9)

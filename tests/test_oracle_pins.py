@@ -196,3 +196,16 @@ class TestSuperres:
             x, tr = R.run_cycling(step, x0, 30, method, objective=cost, reference=truth.ravel())
         assert _rel(x, g[f"sr48/{name}/x"]) <= 1e-10
         _trace_close(tr, g, f"sr48/{name}", rtol=1e-9)
+
+
+def test_product_filter_bank_params_match_oracle():
+    """The product draws the seeded filter-bank parameters itself; they must be
+    bit-identical to the oracle's (host-side, CPU test)."""
+    from paper_1805_02158_b200.denoisers import filter_bank_params
+
+    for seed in (0, 1, 7):
+        k, s, tau = filter_bank_params(seed)
+        ko, so, tauo = extras.filter_bank_params(seed)
+        np.testing.assert_array_equal(k, ko)
+        np.testing.assert_array_equal(s, so)
+        assert tau == tauo
