@@ -214,7 +214,7 @@ struct redve_problem {
   int dn_api_kind = 0;  // REDVE_DN_* as requested
   int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
   double pw_h = 110.0;
-  DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
+  DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg, Z2;
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
   DevBuf rd_filters, rd_scales;
@@ -261,26 +261,43 @@ static int map_dn_kind(int k) {
 }
 
 // Fourier solve pipeline on pairs: Z <- rowfwd(xin) ; col(scale) ; rowinv -> out
-static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double scale, View out,
-                            const double* base, int epilogue, View xprev, StepCtl ctl,
-                            TraceBufs tr, int S, int phase) {
+// The three Fourier kernels as separate pieces (the solve chains row_inv of
+// step k with row_fwd of step k+1 when nothing happens in between).
+static int f_row_fwd(redve_problem* p, View xin, DenoiseArgs dn, cd* Z, int phase) {
   redve_ctx* ctx = p->ctx;
-  RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, p->Z.as<cd>(), p->twW, p->twsW,
+  RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, Z, p->twW, p->twsW,
                 p->state.as<ImgState>(), phase};
   RUN(ctx, "row_fwd", launch_row_fwd(rf, p->npairs, ctx->stream));
   CKL();
-  ColArgs ca{p->B, p->H, p->W, p->lpc_col, p->Z.as<cd>(), p->twH, p->twsH, p->g.as<double>(),
+  return REDVE_OK;
+}
+static int f_col(redve_problem* p, cd* Z, double scale, int phase) {
+  redve_ctx* ctx = p->ctx;
+  ColArgs ca{p->B, p->H, p->W, p->lpc_col, Z, p->twH, p->twsH, p->g.as<double>(),
              scale, p->state.as<ImgState>(), phase};
   RUN(ctx, "col", launch_col(ca, p->npairs, ctx->stream));
   CKL();
+  return REDVE_OK;
+}
+static int f_row_inv(redve_problem* p, const cd* Z, View out, const double* base, int epilogue,
+                     View xprev, StepCtl ctl, TraceBufs tr, int S) {
+  redve_ctx* ctx = p->ctx;
   RowInvArgs ri;
   ri.B = p->B; ri.H = p->H; ri.W = p->W; ri.lpc = p->lpc_row;
-  ri.Z = p->Z.as<cd>(); ri.tw = p->twW; ri.tws = p->twsW; ri.out = out; ri.base = base; ri.xprev = xprev;
+  ri.Z = Z; ri.tw = p->twW; ri.tws = p->twsW; ri.out = out; ri.base = base; ri.xprev = xprev;
   ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
   ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
   RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
   CKL();
   return REDVE_OK;
+}
+static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double scale, View out,
+                            const double* base, int epilogue, View xprev, StepCtl ctl,
+                            TraceBufs tr, int S, int phase) {
+  int r = f_row_fwd(p, xin, dn, p->Z.as<cd>(), phase);
+  if (r) return r;
+  if ((r = f_col(p, p->Z.as<cd>(), scale, phase))) return r;
+  return f_row_inv(p, p->Z.as<cd>(), out, base, epilogue, xprev, ctl, tr, S);
 }
 
 static View plain(const double* base, long long N) {
@@ -1015,22 +1032,47 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     CKL();
   }
 
-  auto step = [&](int phase, bool cadence) -> int {
+  // Z ping-pong: a chained step leaves the next step's row spectrum in zc
+  const bool can_chain = p->fourier && row_inv_fwd_ok(p->W, p->dn_kind) &&
+                         256 / (p->W / 16) - 2 * dn.radius >= 2;
+  if (can_chain) CK(p->Z2.ensure(sizeof(cd) * N * p->npairs));
+  cd* zc = p->Z.as<cd>();
+  cd* zn = can_chain ? p->Z2.as<cd>() : nullptr;
+  bool z_ready = false;
+  auto step = [&](int phase, bool cadence, bool chain) -> int {
     StepCtl c = ctl;
     c.phase = phase;
     c.defer_commit = cadence ? 1 : 0;
-    int r;
+    int r = REDVE_OK;
     if (p->fourier) {
-      View xin = cur;
-      DenoiseArgs d = dn;
-      if (pw) {
-        r = denoise_to_fbuf(p, cur, phase);
-        if (r) return r;
-        xin = plain(p->fbuf.as<double>(), N);
-        d.kind = DN_IDENTITY;
-        d.radius = 0;
+      if (!z_ready) {
+        View xin = cur;
+        DenoiseArgs d = dn;
+        if (pw) {
+          r = denoise_to_fbuf(p, cur, phase);
+          if (r) return r;
+          xin = plain(p->fbuf.as<double>(), N);
+          d.kind = DN_IDENTITY;
+          d.radius = 0;
+        }
+        if ((r = f_row_fwd(p, xin, d, zc, phase))) return r;
       }
-      r = fourier_pipeline(p, xin, d, p->alpha, nxt, p->xb.as<double>(), 1, cur, c, tr, S, phase);
+      if ((r = f_col(p, zc, p->alpha, phase))) return r;
+      if (chain && can_chain) {
+        RowInvFwdArgs fa;
+        fa.B = B; fa.H = p->H; fa.W = p->W;
+        fa.lines = 256 / (p->W / 16);
+        fa.Z = zc; fa.Z2 = zn; fa.tws = p->twsW; fa.out = nxt; fa.base = p->xb.as<double>();
+        fa.xprev = cur; fa.dn = dn; fa.S = S; fa.st = st; fa.ctl = c; fa.tr = tr;
+        fa.partials = p->partials.as<double>(); fa.counters = p->cnt_inv.as<unsigned>();
+        RUN(ctx, "row_inv_fwd", launch_row_inv_fwd(fa, p->npairs, s));
+        CKL();
+        std::swap(zc, zn);
+        z_ready = true;
+      } else {
+        r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
+        z_ready = false;
+      }
     } else {
       r = fp_step_cg(p, cur, nxt, phase, nullptr);
       if (r) return r;
@@ -1065,7 +1107,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   int k = 0;
   if (!ve) {
     while (k < budget) {
-      int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+      int r = step(PH_MAIN, ((k + 1) % log_every) == 0, k + 1 < budget);
       if (r) return r;
       ++k;
       if (k % (check_every * clen) == 0 && k < budget) {
@@ -1079,7 +1121,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     while (true) {
       int n = 0;
       for (int i = 0; i < clen; ++i) {
-        int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+        int r = step(PH_MAIN, ((k + 1) % log_every) == 0, i + 1 < clen && k + 1 < budget);
         if (r) return r;
         ++k;
         ++n;
@@ -1101,8 +1143,9 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
     }
   }
+  z_ready = false;
   for (int i = 0; i < stab; ++i) {
-    int r = step(PH_STAB, true);
+    int r = step(PH_STAB, true, i + 1 < stab);
     if (r) return r;
   }
   if (track) {  // finalize (solvers.py:255-262)
