@@ -1033,7 +1033,9 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   }
 
   // Z ping-pong: a chained step leaves the next step's row spectrum in zc
-  const bool can_chain = p->fourier && row_inv_fwd_ok(p->W, p->dn_kind) &&
+  // the fused inverse+forward row kernel measured slower than the pair it replaces
+  // (83.8 vs 42.3 + 32.1 us at 64 x 256^2: one 256-thread CTA per SM); kept off
+  const bool can_chain = false && p->fourier && row_inv_fwd_ok(p->W, p->dn_kind) &&
                          256 / (p->W / 16) - 2 * dn.radius >= 2;
   if (can_chain) CK(p->Z2.ensure(sizeof(cd) * N * p->npairs));
   cd* zc = p->Z.as<cd>();

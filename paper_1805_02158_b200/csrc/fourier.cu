@@ -218,7 +218,7 @@ void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s) {
 
 // --------------------------------------------------------------- columns
 template <int LH>
-__global__ void __launch_bounds__(256) k_col(ColArgs a) {
+__global__ void __launch_bounds__(128, 4) k_col(ColArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
   const bool a0 = takes_step(a.st[b0], a.phase);
   const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
@@ -295,7 +295,7 @@ void launch_col(const ColArgs& a, int npairs, cudaStream_t s) {
 
 // --------------------------------------------------------------- row inverse
 template <int LW>
-__global__ void __launch_bounds__(256) k_row_inv(RowInvArgs a) {
+__global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
   const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
   const bool a0 = takes_step(a.st[b0], phase);
