@@ -287,7 +287,11 @@ static int f_row_inv(redve_problem* p, const cd* Z, View out, const double* base
   ri.Z = Z; ri.tw = p->twW; ri.tws = p->twsW; ri.out = out; ri.base = base; ri.xprev = xprev;
   ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
   ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
-  RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
+  if (row_inv_pp_ok(p->W, p->lpc_row)) {
+    RUN(ctx, "row_inv", launch_row_inv_pp(ri, p->npairs, ctx->stream));
+  } else {
+    RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
+  }
   CKL();
   return REDVE_OK;
 }

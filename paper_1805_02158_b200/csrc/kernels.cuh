@@ -169,6 +169,9 @@ size_t row_inv_smem(int W, int lpc);
 void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s);
 void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
 void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);
+size_t row_inv_pp_smem(int W, int lpc);
+bool row_inv_pp_ok(int W, int lpc);
+void launch_row_inv_pp(const RowInvArgs& a, int npairs, cudaStream_t s);
 int cost_rows(int H);
 void launch_cost(const CostArgs& a, int npairs, cudaStream_t s);
 bool cost_fast_ok(const CostArgs& a);
