@@ -527,27 +527,35 @@ __global__ void __launch_bounds__(128, 1) k_row_inv_pp(RowInvArgs a) {
         }
       }
     }
-    if (a.epilogue) {
+    if (a.epilogue) {  // partials only: the record runs in k_pair_record (no fences here)
       block_sum<6>(acc, s_red);
       if (threadIdx.x == 0) {
         double* dst = a.partials + ((long long)p * nrb + rb) * 6;
 #pragma unroll
         for (int i = 0; i < 6; ++i) dst[i] = acc[i];
       }
-      __shared__ int s_last;
-      if (last_block_of_group(a.counters + p, nrb, &s_last) && threadIdx.x == 0) {
-        double tot[6] = {0, 0, 0, 0, 0, 0};
-        for (int blk = 0; blk < nrb; ++blk) {
-          const volatile double* src = a.partials + ((long long)p * nrb + blk) * 6;
-          for (int i = 0; i < 6; ++i) tot[i] += src[i];
-        }
-        if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
-        if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
-      }
     }
     __syncthreads();  // this stage is refilled two items from now
   }
   cp_wait<0>();
+}
+
+// Reduce a pair's row-block partials in block order and record the step.
+__global__ void k_pair_record(RowInvArgs a, int nrb) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int npairs = (a.B + 1) / 2;
+  if (p >= npairs) return;
+  const int b0 = 2 * p, b1 = 2 * p + 1;
+  const bool a0 = takes_step(a.st[b0], a.ctl.phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.ctl.phase);
+  if (!a0 && !a1) return;
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  for (int blk = 0; blk < nrb; ++blk) {
+    const double* src = a.partials + ((long long)p * nrb + blk) * 6;
+    for (int i = 0; i < 6; ++i) tot[i] += src[i];
+  }
+  if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
+  if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
 }
 
 static int sm_count() {
@@ -567,6 +575,8 @@ static void row_inv_pp_t(const RowInvArgs& a, int npairs, cudaStream_t s) {
   const int nitems = npairs * ((a.H + a.lpc - 1) / a.lpc);
   const int grid = nitems < sm_count() ? nitems : sm_count();
   k_row_inv_pp<LW><<<grid, a.lpc * (LW / 16), row_inv_pp_smem(LW, a.lpc), s>>>(a);
+  if (a.epilogue)
+    k_pair_record<<<(npairs + 127) / 128, 128, 0, s>>>(a, (a.H + a.lpc - 1) / a.lpc);
 }
 
 bool row_inv_pp_ok(int W, int lpc) {
