@@ -214,7 +214,7 @@ struct redve_problem {
   int dn_api_kind = 0;  // REDVE_DN_* as requested
   int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
   double pw_h = 110.0;
-  DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg, Z2;
+  DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
   DevBuf rd_filters, rd_scales;
@@ -261,8 +261,7 @@ static int map_dn_kind(int k) {
 }
 
 // Fourier solve pipeline on pairs: Z <- rowfwd(xin) ; col(scale) ; rowinv -> out
-// The three Fourier kernels as separate pieces (the solve chains row_inv of
-// step k with row_fwd of step k+1 when nothing happens in between).
+// The three Fourier kernels as separate pieces.
 static int f_row_fwd(redve_problem* p, View xin, DenoiseArgs dn, cd* Z, int phase) {
   redve_ctx* ctx = p->ctx;
   RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, Z, p->twW, p->twsW,
@@ -287,11 +286,7 @@ static int f_row_inv(redve_problem* p, const cd* Z, View out, const double* base
   ri.Z = Z; ri.tw = p->twW; ri.tws = p->twsW; ri.out = out; ri.base = base; ri.xprev = xprev;
   ri.epilogue = epilogue; ri.S = S; ri.st = p->state.as<ImgState>(); ri.ctl = ctl; ri.tr = tr;
   ri.partials = p->partials.as<double>(); ri.counters = p->cnt_inv.as<unsigned>();
-  if (row_inv_pp_ok(p->W, p->lpc_row)) {
-    RUN(ctx, "row_inv", launch_row_inv_pp(ri, p->npairs, ctx->stream));
-  } else {
-    RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
-  }
+  RUN(ctx, "row_inv", launch_row_inv(ri, p->npairs, ctx->stream));
   CKL();
   return REDVE_OK;
 }
@@ -1036,22 +1031,14 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     CKL();
   }
 
-  // Z ping-pong: a chained step leaves the next step's row spectrum in zc
-  // the fused inverse+forward row kernel measured slower than the pair it replaces
-  // (83.8 vs 42.3 + 32.1 us at 64 x 256^2: one 256-thread CTA per SM); kept off
-  const bool can_chain = false && p->fourier && row_inv_fwd_ok(p->W, p->dn_kind) &&
-                         256 / (p->W / 16) - 2 * dn.radius >= 2;
-  if (can_chain) CK(p->Z2.ensure(sizeof(cd) * N * p->npairs));
   cd* zc = p->Z.as<cd>();
-  cd* zn = can_chain ? p->Z2.as<cd>() : nullptr;
-  bool z_ready = false;
-  auto step = [&](int phase, bool cadence, bool chain) -> int {
+  auto step = [&](int phase, bool cadence) -> int {
     StepCtl c = ctl;
     c.phase = phase;
     c.defer_commit = cadence ? 1 : 0;
     int r = REDVE_OK;
     if (p->fourier) {
-      if (!z_ready) {
+      {
         View xin = cur;
         DenoiseArgs d = dn;
         if (pw) {
@@ -1064,21 +1051,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         if ((r = f_row_fwd(p, xin, d, zc, phase))) return r;
       }
       if ((r = f_col(p, zc, p->alpha, phase))) return r;
-      if (chain && can_chain) {
-        RowInvFwdArgs fa;
-        fa.B = B; fa.H = p->H; fa.W = p->W;
-        fa.lines = 256 / (p->W / 16);
-        fa.Z = zc; fa.Z2 = zn; fa.tws = p->twsW; fa.out = nxt; fa.base = p->xb.as<double>();
-        fa.xprev = cur; fa.dn = dn; fa.S = S; fa.st = st; fa.ctl = c; fa.tr = tr;
-        fa.partials = p->partials.as<double>(); fa.counters = p->cnt_inv.as<unsigned>();
-        RUN(ctx, "row_inv_fwd", launch_row_inv_fwd(fa, p->npairs, s));
-        CKL();
-        std::swap(zc, zn);
-        z_ready = true;
-      } else {
-        r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
-        z_ready = false;
-      }
+      r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
     } else {
       r = fp_step_cg(p, cur, nxt, phase, nullptr);
       if (r) return r;
@@ -1113,7 +1086,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   int k = 0;
   if (!ve) {
     while (k < budget) {
-      int r = step(PH_MAIN, ((k + 1) % log_every) == 0, k + 1 < budget);
+      int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
       if (r) return r;
       ++k;
       if (k % (check_every * clen) == 0 && k < budget) {
@@ -1127,7 +1100,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     while (true) {
       int n = 0;
       for (int i = 0; i < clen; ++i) {
-        int r = step(PH_MAIN, ((k + 1) % log_every) == 0, i + 1 < clen && k + 1 < budget);
+        int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
         if (r) return r;
         ++k;
         ++n;
@@ -1149,9 +1122,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
     }
   }
-  z_ready = false;
   for (int i = 0; i < stab; ++i) {
-    int r = step(PH_STAB, true, i + 1 < stab);
+    int r = step(PH_STAB, true);
     if (r) return r;
   }
   if (track) {  // finalize (solvers.py:255-262)

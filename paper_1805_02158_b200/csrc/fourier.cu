@@ -16,7 +16,6 @@
 // anything else the runtime plan (direct DFT for non powers of two).
 #include "cost.cuh"
 #include "kernels.cuh"
-#include "pipeline.cuh"
 
 namespace redve {
 
@@ -412,338 +411,6 @@ void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s) {
     case 512: row_inv_t<512>(a, npairs, s); break;
     case 1024: row_inv_t<1024>(a, npairs, s); break;
     default: row_inv_t<0>(a, npairs, s); break;
-  }
-}
-
-// --------------------------------------------------------------- persistent inverse rows
-// One CTA per SM loops over (pair, row block) items; while item i is
-// transformed in shared memory, item i+1's inputs (spectrum rows, x_b rows,
-// x_k rows) are already in flight with cp.async, so the HBM/L2 latency that
-// serialised the one-shot kernel is hidden behind the FFT.
-static size_t rip_stage_bytes(int W, int lpc) {
-  return (size_t)lpc * RowLayout::stride_for(W) * sizeof(cd) + 4ull * lpc * W * sizeof(double);
-}
-size_t row_inv_pp_smem(int W, int lpc) {
-  return tw_bytes(W) + 2 * rip_stage_bytes(W, lpc) + al16f(32 * 6 * sizeof(double));
-}
-
-template <int LW>
-__global__ void __launch_bounds__(128, 1) k_row_inv_pp(RowInvArgs a) {
-  constexpr int W = LW, T = LW / 16, W2 = LW / 2;
-  constexpr int ntw = tw_stage_size(LW);
-  const int H = a.H, lpc = a.lpc;
-  const long long N = (long long)H * W;
-  const int nrb = (H + lpc - 1) / lpc;
-  const int npairs = (a.B + 1) / 2;
-  const int nitems = npairs * nrb;
-  const int stride = RowLayout::stride_for(W);
-  const size_t stage = (size_t)lpc * stride * sizeof(cd) + 4ull * lpc * W * sizeof(double);
-  cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  unsigned char* st0 = f_smem + al16f(ntw * sizeof(cd));
-  double* s_red = reinterpret_cast<double*>(st0 + 2 * stage);
-  load_twiddles(s_tw, a.tws, ntw);
-  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
-  const RowLayout lay{stride};
-  auto zs_of = [&](int sidx) { return reinterpret_cast<cd*>(st0 + sidx * stage); };
-  auto xs_of = [&](int sidx) {
-    return reinterpret_cast<double*>(st0 + sidx * stage + (size_t)lpc * stride * sizeof(cd));
-  };
-  auto issue = [&](int item, int sidx) {
-    const int p = item / nrb, rb = item - p * nrb, r0 = rb * lpc;
-    const int b0 = 2 * p, b1 = 2 * p + 1;
-    const bool a0 = takes_step(a.st[b0], phase);
-    const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
-    if (a0 || a1) {
-      cd* zs = zs_of(sidx);
-      double* xs = xs_of(sidx);
-      for (int e = threadIdx.x; e < lpc * W; e += blockDim.x) {
-        const int line = e / W, c = e - line * W, row = r0 + line;
-        if (row < H) cp16(zs + lay.at(line, c), a.Z + ((long long)p * H + row) * W + c);
-      }
-      const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N : nullptr;
-      const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N : nullptr;
-      const double* p0 = (a0 && a.epilogue) ? a.xprev.at(b0, a.st) : nullptr;
-      const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) : nullptr;
-      for (int e = threadIdx.x; e < lpc * W2; e += blockDim.x) {
-        const int line = e / W2, c = 2 * (e - line * W2), row = r0 + line;
-        if (row >= H) continue;
-        const long long o = (long long)row * W + c;
-        double* d = xs + line * W + c;
-        if (bs0) cp16(d, bs0 + o);
-        if (bs1) cp16(d + lpc * W, bs1 + o);
-        if (p0) cp16(d + 2 * lpc * W, p0 + o);
-        if (p1) cp16(d + 3 * lpc * W, p1 + o);
-      }
-    }
-    cp_commit();
-  };
-  int item = blockIdx.x;
-  if (item < nitems) issue(item, 0);
-  else cp_commit();
-  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
-  for (int sidx = 0; item < nitems; item += gridDim.x, sidx ^= 1) {
-    const int next = item + gridDim.x;
-    if (next < nitems) issue(next, sidx ^ 1);
-    else cp_commit();
-    cp_wait<1>();
-    __syncthreads();
-    const int p = item / nrb, rb = item - p * nrb;
-    const int b0 = 2 * p, b1 = 2 * p + 1;
-    const bool a0 = takes_step(a.st[b0], phase);
-    const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
-    if (!a0 && !a1) continue;  // uniform across the CTA
-    cd* zs = zs_of(sidx);
-    const double* xs = xs_of(sidx);
-    cd v[16];
-    line_fft_ct<LW, true, true>(v, zs, s_tw, t, line, lay);
-    const int row = rb * lpc + line;
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    if (row < H) {
-      double* o0 = a0 ? a.out.at(b0, a.st) + (long long)row * W : nullptr;
-      double* o1 = a1 ? a.out.at(b1, a.st) + (long long)row * W : nullptr;
-      const double* xl = xs + line * W;
-#pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        const int c = t + T * m;
-        if (o0) {
-          const double val = v[m].x + (a.base ? xl[c] : 0.0);
-          o0[c] = val;
-          if (a.epilogue) {
-            const double xp = xl[c + 2 * lpc * W], d = val - xp;
-            acc[0] = fma(d, d, acc[0]);
-            acc[1] = fma(xp, xp, acc[1]);
-            acc[2] += isfinite(val) ? 0.0 : 1.0;
-          }
-        }
-        if (o1) {
-          const double val = v[m].y + (a.base ? xl[c + lpc * W] : 0.0);
-          o1[c] = val;
-          if (a.epilogue) {
-            const double xp = xl[c + 3 * lpc * W], d = val - xp;
-            acc[3] = fma(d, d, acc[3]);
-            acc[4] = fma(xp, xp, acc[4]);
-            acc[5] += isfinite(val) ? 0.0 : 1.0;
-          }
-        }
-      }
-    }
-    if (a.epilogue) {  // partials only: the record runs in k_pair_record (no fences here)
-      block_sum<6>(acc, s_red);
-      if (threadIdx.x == 0) {
-        double* dst = a.partials + ((long long)p * nrb + rb) * 6;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) dst[i] = acc[i];
-      }
-    }
-    __syncthreads();  // this stage is refilled two items from now
-  }
-  cp_wait<0>();
-}
-
-// Reduce a pair's row-block partials in block order and record the step.
-__global__ void k_pair_record(RowInvArgs a, int nrb) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int npairs = (a.B + 1) / 2;
-  if (p >= npairs) return;
-  const int b0 = 2 * p, b1 = 2 * p + 1;
-  const bool a0 = takes_step(a.st[b0], a.ctl.phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.ctl.phase);
-  if (!a0 && !a1) return;
-  double tot[6] = {0, 0, 0, 0, 0, 0};
-  for (int blk = 0; blk < nrb; ++blk) {
-    const double* src = a.partials + ((long long)p * nrb + blk) * 6;
-    for (int i = 0; i < 6; ++i) tot[i] += src[i];
-  }
-  if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
-  if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
-}
-
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
-
-template <int LW>
-static void row_inv_pp_t(const RowInvArgs& a, int npairs, cudaStream_t s) {
-  static bool done = false;
-  big_smem_once(k_row_inv_pp<LW>, done);
-  const int nitems = npairs * ((a.H + a.lpc - 1) / a.lpc);
-  const int grid = nitems < sm_count() ? nitems : sm_count();
-  k_row_inv_pp<LW><<<grid, a.lpc * (LW / 16), row_inv_pp_smem(LW, a.lpc), s>>>(a);
-  if (a.epilogue)
-    k_pair_record<<<(npairs + 127) / 128, 128, 0, s>>>(a, (a.H + a.lpc - 1) / a.lpc);
-}
-
-bool row_inv_pp_ok(int W, int lpc) {
-  return (W == 64 || W == 128 || W == 256 || W == 512) && row_inv_pp_smem(W, lpc) <= 220 * 1024;
-}
-
-void launch_row_inv_pp(const RowInvArgs& a, int npairs, cudaStream_t s) {
-  switch (a.W) {
-    case 64: row_inv_pp_t<64>(a, npairs, s); break;
-    case 128: row_inv_pp_t<128>(a, npairs, s); break;
-    case 256: row_inv_pp_t<256>(a, npairs, s); break;
-    default: row_inv_pp_t<512>(a, npairs, s); break;
-  }
-}
-
-// --------------------------------------------------------------- fused inverse + forward rows
-size_t row_inv_fwd_smem(int W, int lines, int ksize) {
-  return tw_bytes(W) + al16f((size_t)ksize * ksize * sizeof(double)) +
-         (size_t)lines * RowLayout::stride_for(W) * sizeof(cd) + al16f(32 * 6 * sizeof(double));
-}
-bool row_inv_fwd_ok(int W, int dn_kind) {
-  return ct_size(W) && W >= 64 && dn_kind != DN_EXTERNAL;
-}
-
-template <int LW, int DK>
-__global__ void __launch_bounds__(256, 2) k_row_inv_fwd(RowInvFwdArgs a) {
-  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const bool a0 = takes_step(a.st[b0], a.ctl.phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], a.ctl.phase);
-  if (!a0 && !a1) return;
-  constexpr int W = LW, T = LW / 16;
-  const int H = a.H;
-  const long long N = (long long)H * W;
-  const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
-  const int ks = DK == DN_CONV ? a.dn.ksize : 0;
-  const int lpc = a.lines - 2 * R;
-  constexpr int ntw = tw_stage_size(LW);
-  cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  double* s_taps = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)));
-  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)) +
-                                     al16f((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
-  double* s_red = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_work) +
-                                            (size_t)a.lines * RowLayout::stride_for(W) * sizeof(cd));
-  load_twiddles(s_tw, a.tws, ntw);
-  if (DK == DN_CONV)
-    for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
-  const int line = threadIdx.x / T, t = threadIdx.x - line * T;
-  const int r0 = blockIdx.x * lpc;
-  const int urow = r0 - R + line;                 // unwrapped row of this line
-  const int row = wrap(urow, H);
-  const bool own = line >= R && line < R + lpc && urow < H;
-  const cd* zr = a.Z + ((long long)p * H + row) * W;
-  cd v[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = ld_cd(zr + t + T * m);
-  __syncthreads();
-  RowLayout lay{RowLayout::stride_for(W)};
-  line_fft_ct<LW, true>(v, s_work, s_tw, t, line, lay);  // ends with all smem reads done
-
-  // x+ = IDFT + x_b for every line (tile incl. halo); own lines: write + step norm
-  const double* bs0 = a0 ? a.base + (long long)b0 * N + (long long)row * W : nullptr;
-  const double* bs1 = a1 ? a.base + (long long)b1 * N + (long long)row * W : nullptr;
-  double* o0 = (a0 && own) ? a.out.at(b0, a.st) + (long long)row * W : nullptr;
-  double* o1 = (a1 && own) ? a.out.at(b1, a.st) + (long long)row * W : nullptr;
-  const double* p0 = (a0 && own) ? a.xprev.at(b0, a.st) + (long long)row * W : nullptr;
-  const double* p1 = (a1 && own) ? a.xprev.at(b1, a.st) + (long long)row * W : nullptr;
-  double acc[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double lb0[8], lb1[8], lp0[8], lp1[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = t + T * (8 * h + q);
-      lb0[q] = bs0 ? __ldg(bs0 + c) : 0.0;
-      lb1[q] = bs1 ? __ldg(bs1 + c) : 0.0;
-      lp0[q] = p0 ? __ldg(p0 + c) : 0.0;
-      lp1[q] = p1 ? __ldg(p1 + c) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int m = 8 * h + q;
-      const int c = t + T * m;
-      const double v0 = v[m].x + lb0[q], v1 = v[m].y + lb1[q];
-      st_cd(s_work + lay.at(line, c), cd{v0, v1});
-      if (o0) {
-        o0[c] = v0;
-        const double d = v0 - lp0[q];
-        acc[0] = fma(d, d, acc[0]);
-        acc[1] = fma(lp0[q], lp0[q], acc[1]);
-        acc[2] += isfinite(v0) ? 0.0 : 1.0;
-      }
-      if (o1) {
-        o1[c] = v1;
-        const double d = v1 - lp1[q];
-        acc[3] = fma(d, d, acc[3]);
-        acc[4] = fma(lp1[q], lp1[q], acc[4]);
-        acc[5] += isfinite(v1) ? 0.0 : 1.0;
-      }
-    }
-  }
-  __syncthreads();
-  // f(x+) over the own lines, contiguous spans; halo lines only feed the stencil
-  const TileLayout tl{RowLayout::stride_for(W)};
-  const int c0 = 16 * t;
-  cd f[16];
-  if (own) {
-    denoise_span<DK>(f, s_work, tl, line, c0, ks, s_taps, [&](int c) { return edge_wrap(c, W); });
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) f[j] = cd{0.0, 0.0};
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < 16; ++j) st_cd(s_work + lay.at(line, c0 + j), f[j]);
-  __syncthreads();
-  line_fft_ct<LW, false, true>(v, s_work, s_tw, t, line, lay);
-  if (own) {
-    cd* z2 = a.Z2 + ((long long)p * H + row) * W;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) st_cd(z2 + t + T * m, v[m]);
-  }
-  // step record for x+ (as k_row_inv)
-  block_sum<6>(acc, s_red);
-  const int nblk = gridDim.x;
-  if (threadIdx.x == 0) {
-    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
-  }
-  __shared__ int s_last;
-  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
-      for (int i = 0; i < 6; ++i) tot[i] += src[i];
-    }
-    if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
-    if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
-  }
-}
-
-template <int LW, int DK>
-static void row_inv_fwd_t(const RowInvFwdArgs& a, int npairs, cudaStream_t s) {
-  static bool done = false;
-  big_smem_once(k_row_inv_fwd<LW, DK>, done);
-  const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
-  const int lpc = a.lines - 2 * R;
-  dim3 grid(cdivf(a.H, lpc), npairs);
-  k_row_inv_fwd<LW, DK><<<grid, a.lines * (LW / 16), row_inv_fwd_smem(LW, a.lines, a.dn.ksize), s>>>(a);
-}
-
-template <int DK>
-static void row_inv_fwd_dk(const RowInvFwdArgs& a, int npairs, cudaStream_t s) {
-  switch (a.W) {
-    case 64: row_inv_fwd_t<64, DK>(a, npairs, s); break;
-    case 128: row_inv_fwd_t<128, DK>(a, npairs, s); break;
-    case 256: row_inv_fwd_t<256, DK>(a, npairs, s); break;
-    case 512: row_inv_fwd_t<512, DK>(a, npairs, s); break;
-    default: row_inv_fwd_t<1024, DK>(a, npairs, s); break;
-  }
-}
-
-void launch_row_inv_fwd(const RowInvFwdArgs& a, int npairs, cudaStream_t s) {
-  switch (a.dn.kind) {
-    case DN_CONV: row_inv_fwd_dk<DN_CONV>(a, npairs, s); break;
-    case DN_MEDIAN3: row_inv_fwd_dk<DN_MEDIAN3>(a, npairs, s); break;
-    default: row_inv_fwd_dk<DN_IDENTITY>(a, npairs, s); break;
   }
 }
 

@@ -47,29 +47,6 @@ struct RowInvArgs {
   unsigned* counters;
 };
 
-// Fused inverse row pass of step k + forward row pass of step k+1 (same rows):
-// Z -> x+ (written, recorded) -> f(x+) -> row FFTs -> Z2.  Each CTA inverse-
-// transforms lpc + 2R lines so the denoiser has its halo rows in shared memory.
-struct RowInvFwdArgs {
-  int B, H, W, lines;  // lines per CTA = lpc + 2R
-  const cd* Z;
-  cd* Z2;
-  const cd* tws;
-  View out;            // x+ (next ring slot)
-  const double* base;  // x_b
-  View xprev;          // x_k
-  DenoiseArgs dn;
-  int S;
-  ImgState* st;
-  StepCtl ctl;
-  TraceBufs tr;
-  double* partials;
-  unsigned* counters;
-};
-size_t row_inv_fwd_smem(int W, int lines, int ksize);
-bool row_inv_fwd_ok(int W, int dn_kind);
-void launch_row_inv_fwd(const RowInvFwdArgs& a, int npairs, cudaStream_t s);
-
 enum CostMode : int { COST_RECORD = 0, COST_INIT = 1, COST_FINAL = 2, COST_VALUE = 3 };
 
 struct CostArgs {
@@ -169,9 +146,6 @@ size_t row_inv_smem(int W, int lpc);
 void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s);
 void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
 void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);
-size_t row_inv_pp_smem(int W, int lpc);
-bool row_inv_pp_ok(int W, int lpc);
-void launch_row_inv_pp(const RowInvArgs& a, int npairs, cudaStream_t s);
 int cost_rows(int H);
 void launch_cost(const CostArgs& a, int npairs, cudaStream_t s);
 bool cost_fast_ok(const CostArgs& a);
