@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -97,6 +98,8 @@ struct ProfEvent {
 
 struct redve_ctx {
   bool profiling = false;
+  cudaStream_t cap_stream = nullptr;  // graph capture
+  cudaEvent_t fork_ev = nullptr;
   std::vector<ProfEvent> prof;
   std::vector<cudaEvent_t> ev_pool;
   int device = 0;
@@ -198,6 +201,11 @@ static int fail(redve_ctx* c, int code, const char* fmt, ...) {
 
 static int is_odd_pos(int k) { return k >= 1 && (k & 1); }
 
+static bool graphs_enabled() {
+  const char* e = getenv("REDVE_GRAPHS");
+  return !(e && e[0] == '0');
+}
+
 // ------------------------------------------------------------------ problem
 struct redve_problem {
   redve_ctx* ctx;
@@ -215,6 +223,12 @@ struct redve_problem {
   int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
   double pw_h = 110.0;
   DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
+  cudaGraphExec_t gexec = nullptr;  // captured solve (Fourier route)
+  std::string gkey;
+  unsigned long long glaunches = 0;
+  ~redve_problem() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
   DevBuf rd_filters, rd_scales;
@@ -921,7 +935,7 @@ int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* c
 int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x0, double* x_out,
                 redve_trace* trace) {
   redve_ctx* ctx = p->ctx;
-  const cudaStream_t s = ctx->stream;
+  cudaStream_t s = ctx->stream;
   if (cfg->method != REDVE_METHOD_FP && cfg->method != REDVE_METHOD_FP_VE)
     return fail(ctx, REDVE_E_VALUE, "unknown method %d", cfg->method);
   if (cfg->ve_method < 0 || cfg->ve_method > 2) return fail(ctx, REDVE_E_VALUE, "unknown VE method");
@@ -987,154 +1001,200 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     tr.cyc_c = tr.cyc_gamma + ncyc * MAXKP1;
     tr.cyc_meta = reinterpret_cast<int*>(tr.cyc_c + ncyc * MAXKP1);
   }
-  CK(cudaMemsetAsync(p->trace.p, 0xFF, sizeof(double) * 5 * nrec, s));  // NaN
-  CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
-                                         sizeof(int) * ncyc * 4, s));
-  ImgState* st = p->state.as<ImgState>();
-  RUN(ctx, "init_state", launch_init_state(st, B, s));
-  CKL();
-  // x0 -> ring slot 0
-  CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * N * S, x0, sizeof(double) * N,
-                       sizeof(double) * N, B, cudaMemcpyDeviceToDevice, s));
-
-  View cur{p->ring.as<double>(), N * S, N, S, 1};
-  View nxt{p->ring.as<double>(), N * S, N, S, 2};
-  View bestv = plain(p->best.as<double>(), N);
-  DenoiseArgs dn = dn_args(p);
-  StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0};
-
-  VeArgs va;
-  va.B = B; va.N = N; va.m = cfg->m; va.kp1 = kp1; va.S = S;
-  va.ring = p->ring.as<double>(); va.img_stride = N * S; va.slot_stride = N;
-  va.st = st; va.tr = tr; va.partials = p->partials.as<double>();
-  va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
-  va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
-
-  // cost evaluation of the current iterates: PatchWeighted needs f(x) first
-  auto cost_of_cur = [&](int mode, StepCtl c) -> int {
-    const double* fe = nullptr;
-    if (pw) {
-      int r = denoise_to_fbuf(p, cur, mode == COST_RECORD ? c.phase : PH_SETUP);
-      if (r) return r;
-      fe = p->fbuf.as<double>();
-    }
-    CostArgs ca = cost_args(p, cur, fe, mode, c, tr);
-    RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
+  // All device work of the solve.  Fourier route with tol == 0 has no host
+  // decision inside, so it is captured once into a CUDA graph and replayed
+  // (the CG route checks its per-image stop flags on the host).
+  const bool use_graph = p->fourier && cfg->tol == 0 && !ctx->profiling && graphs_enabled();
+  char keybuf[512];
+  snprintf(keybuf, sizeof(keybuf), "%p|%p|%p|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%p|%p", (void*)p,
+           (const void*)x0, (void*)x_out, cfg->method, cfg->ve_method, cfg->m, cfg->kappa,
+           cfg->max_inner_steps, cfg->tol, cfg->stabilization_iters, cfg->rank_tolerance,
+           p->ring.p, p->trace.p);
+  auto device_work = [&]() -> int {
+    CK(cudaMemsetAsync(p->trace.p, 0xFF, sizeof(double) * 5 * nrec, s));  // NaN
+    CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
+                                           sizeof(int) * ncyc * 4, s));
+    ImgState* st = p->state.as<ImgState>();
+    RUN(ctx, "init_state", launch_init_state(st, B, s));
     CKL();
-    return REDVE_OK;
-  };
+    // x0 -> ring slot 0
+    CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * N * S, x0, sizeof(double) * N,
+                         sizeof(double) * N, B, cudaMemcpyDeviceToDevice, s));
 
-  if (track) {  // note_initial (solvers.py:219-223)
-    int r0 = cost_of_cur(COST_INIT, ctl);
-    if (r0) return r0;
-    RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
-    CKL();
-  }
+    View cur{p->ring.as<double>(), N * S, N, S, 1};
+    View nxt{p->ring.as<double>(), N * S, N, S, 2};
+    View bestv = plain(p->best.as<double>(), N);
+    DenoiseArgs dn = dn_args(p);
+    StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0};
 
-  cd* zc = p->Z.as<cd>();
-  auto step = [&](int phase, bool cadence) -> int {
-    StepCtl c = ctl;
-    c.phase = phase;
-    c.defer_commit = cadence ? 1 : 0;
-    int r = REDVE_OK;
-    if (p->fourier) {
-      {
-        View xin = cur;
-        DenoiseArgs d = dn;
-        if (pw) {
-          r = denoise_to_fbuf(p, cur, phase);
-          if (r) return r;
-          xin = plain(p->fbuf.as<double>(), N);
-          d.kind = DN_IDENTITY;
-          d.radius = 0;
-        }
-        if ((r = f_row_fwd(p, xin, d, zc, phase))) return r;
+    VeArgs va;
+    va.B = B; va.N = N; va.m = cfg->m; va.kp1 = kp1; va.S = S;
+    va.ring = p->ring.as<double>(); va.img_stride = N * S; va.slot_stride = N;
+    va.st = st; va.tr = tr; va.partials = p->partials.as<double>();
+    va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
+    va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
+
+    // cost evaluation of the current iterates: PatchWeighted needs f(x) first
+    auto cost_of_cur = [&](int mode, StepCtl c) -> int {
+      const double* fe = nullptr;
+      if (pw) {
+        int r = denoise_to_fbuf(p, cur, mode == COST_RECORD ? c.phase : PH_SETUP);
+        if (r) return r;
+        fe = p->fbuf.as<double>();
       }
-      if ((r = f_col(p, zc, p->alpha, phase))) return r;
-      r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
-    } else {
-      r = fp_step_cg(p, cur, nxt, phase, nullptr);
-      if (r) return r;
-      RecordArgs ra;
-      ra.N = N; ra.xnew = nxt; ra.xprev = cur; ra.S = S; ra.st = st; ra.ctl = c; ra.tr = tr;
-      ra.partials = p->part_cg.as<double>(); ra.counters = p->cnt_rec.as<unsigned>();
-      RUN(ctx, "step_record", launch_step_record(ra, B, s));
+      CostArgs ca = cost_args(p, cur, fe, mode, c, tr);
+      RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
+      CKL();
+      return REDVE_OK;
+    };
+
+    if (track) {  // note_initial (solvers.py:219-223)
+      int r0 = cost_of_cur(COST_INIT, ctl);
+      if (r0) return r0;
+      RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
       CKL();
     }
-    if (r) return r;
-    if (cadence) {
-      r = cost_of_cur(COST_RECORD, c);
-      if (r) return r;
-      if (track) {
-        RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
+
+    cd* zc = p->Z.as<cd>();
+    auto step = [&](int phase, bool cadence) -> int {
+      StepCtl c = ctl;
+      c.phase = phase;
+      c.defer_commit = cadence ? 1 : 0;
+      int r = REDVE_OK;
+      if (p->fourier) {
+        {
+          View xin = cur;
+          DenoiseArgs d = dn;
+          if (pw) {
+            r = denoise_to_fbuf(p, cur, phase);
+            if (r) return r;
+            xin = plain(p->fbuf.as<double>(), N);
+            d.kind = DN_IDENTITY;
+            d.radius = 0;
+          }
+          if ((r = f_row_fwd(p, xin, d, zc, phase))) return r;
+        }
+        if ((r = f_col(p, zc, p->alpha, phase))) return r;
+        r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
+      } else {
+        r = fp_step_cg(p, cur, nxt, phase, nullptr);
+        if (r) return r;
+        RecordArgs ra;
+        ra.N = N; ra.xnew = nxt; ra.xprev = cur; ra.S = S; ra.st = st; ra.ctl = c; ra.tr = tr;
+        ra.partials = p->part_cg.as<double>(); ra.counters = p->cnt_rec.as<unsigned>();
+        RUN(ctx, "step_record", launch_step_record(ra, B, s));
         CKL();
       }
-    }
-    return REDVE_OK;
-  };
-
-  std::vector<ImgState> hst(B);
-  auto any_running = [&]() -> int {
-    CK(cudaMemcpyAsync(hst.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    int any = 0;
-    for (int b = 0; b < B; ++b) any |= (hst[b].term == RUNNING);
-    return any ? 1 : 0;
-  };
-  const int check_every = (cfg->tol > 0 || !p->fourier) ? 1 : 8;  // CG steps stop exactly
-
-  int k = 0;
-  if (!ve) {
-    while (k < budget) {
-      int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
       if (r) return r;
-      ++k;
-      if (k % (check_every * clen) == 0 && k < budget) {
-        int a = any_running();
-        if (a < 0 || a > 1) return a;
-        if (!a) break;
+      if (cadence) {
+        r = cost_of_cur(COST_RECORD, c);
+        if (r) return r;
+        if (track) {
+          RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
+          CKL();
+        }
       }
-    }
-  } else {
-    int cycles = 0;
-    while (true) {
-      int n = 0;
-      for (int i = 0; i < clen; ++i) {
+      return REDVE_OK;
+    };
+
+    std::vector<ImgState> hst(B);
+    auto any_running = [&]() -> int {
+      CK(cudaMemcpyAsync(hst.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      int any = 0;
+      for (int b = 0; b < B; ++b) any |= (hst[b].term == RUNNING);
+      return any ? 1 : 0;
+    };
+    const int check_every = (cfg->tol > 0 || !p->fourier) ? 1 : 8;  // CG steps stop exactly
+
+    int k = 0;
+    if (!ve) {
+      while (k < budget) {
         int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
         if (r) return r;
         ++k;
-        ++n;
+        if (!use_graph && k % (check_every * clen) == 0 && k < budget) {
+          int a = any_running();
+          if (a < 0 || a > 1) return a;
+          if (!a) break;
+        }
+      }
+    } else {
+      int cycles = 0;
+      while (true) {
+        int n = 0;
+        for (int i = 0; i < clen; ++i) {
+          int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+          if (r) return r;
+          ++k;
+          ++n;
+          if (k >= budget) break;
+        }
+        if (n == clen) {
+          RUN(ctx, "gram", launch_gram(va, s));
+          CKL();
+          RUN(ctx, "mgs", launch_mgs(va, s));
+          CKL();
+          RUN(ctx, "combine", launch_combine(va, s));
+          CKL();
+        }
         if (k >= budget) break;
-      }
-      if (n == clen) {
-        RUN(ctx, "gram", launch_gram(va, s));
-        CKL();
-        RUN(ctx, "mgs", launch_mgs(va, s));
-        CKL();
-        RUN(ctx, "combine", launch_combine(va, s));
-        CKL();
-      }
-      if (k >= budget) break;
-      if (++cycles % check_every == 0) {
-        int a = any_running();
-        if (a < 0 || a > 1) return a;
-        if (!a) break;
+        if (++cycles % check_every == 0 && !use_graph) {
+          int a = any_running();
+          if (a < 0 || a > 1) return a;
+          if (!a) break;
+        }
       }
     }
-  }
-  for (int i = 0; i < stab; ++i) {
-    int r = step(PH_STAB, true);
+    for (int i = 0; i < stab; ++i) {
+      int r = step(PH_STAB, true);
+      if (r) return r;
+    }
+    if (track) {  // finalize (solvers.py:255-262)
+      int r = cost_of_cur(COST_FINAL, ctl);
+      if (r) return r;
+    }
+    RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s));
+    CKL();
+
+    return REDVE_OK;
+  };
+  if (use_graph && p->gexec && p->gkey == keybuf) {
+    CK(cudaGraphLaunch(p->gexec, s));
+    g_launches.fetch_add(p->glaunches);
+  } else if (use_graph) {
+    const cudaStream_t orig = s;
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    if (!ctx->fork_ev) CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->fork_ev, orig));
+    CK(cudaStreamWaitEvent(ctx->cap_stream, ctx->fork_ev, 0));
+    s = ctx->cap_stream;
+    ctx->stream = s;
+    const unsigned long long l0 = g_launches.load();
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int r = device_work();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    ctx->stream = orig;
+    s = orig;
+    if (r) return r;
+    if (ce != cudaSuccess) return fail(ctx, REDVE_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+    ce = cudaGraphInstantiate(&p->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(ctx, REDVE_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    p->gkey = keybuf;
+    p->glaunches = g_launches.load() - l0;
+    CK(cudaGraphLaunch(p->gexec, s));
+  } else {
+    int r = device_work();
     if (r) return r;
   }
-  if (track) {  // finalize (solvers.py:255-262)
-    int r = cost_of_cur(COST_FINAL, ctl);
-    if (r) return r;
-  }
-  RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s));
-  CKL();
 
   // trace back to the host
-  CK(cudaMemcpyAsync(hst.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
+  std::vector<ImgState> hst(B);
+  CK(cudaMemcpyAsync(hst.data(), p->state.p, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
   const int hc = trace->cap < cap ? trace->cap : cap;
   const int hcc = trace->ccap < ccap ? trace->ccap : ccap;
   auto cp2 = [&](void* dst, const void* src, size_t elem, int hcols, int dcols) -> cudaError_t {
