@@ -1,19 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: RED-FP+MPE image solves/s, BASELINE.json configs[1] workload.
+"""Benchmark: RED-FP+MPE image solves/s on the BASELINE.json configs.
 
-Workload (one "step"): a batch of 64 seeded 256x256 Voronoi scenes, 9x9
-uniform circular blur, noise sigma = sqrt(2), 3x3 median denoiser,
-alpha = 0.02, FP+MPE with m = 0, kappa = 5, 200 baseline evaluations, tol 0
-(the reference defaults, cli.py:60-61,126-129,148), fp64 throughout.  Each
-GPU solves its own batch (weak scaling, no collectives: the images are
-independent).  The timed region is the device-resident solve of the batch
-(inputs already in HBM); ``e2e`` is the same metric through the public API
-with host numpy buffers (problem setup + H2D + solve + D2H of solutions and
-traces inside the timed region).
+Default workload (one "step", BASELINE.json configs[1], the metric's config):
+a batch of 64 seeded 256x256 Voronoi scenes, 9x9 uniform circular blur, noise
+sigma = sqrt(2), 3x3 median denoiser, alpha = 0.02, FP+MPE with m = 0,
+kappa = 5, 200 baseline evaluations, tol 0 (the reference defaults,
+cli.py:60-61,126-129,148), fp64 throughout.  Each GPU solves its own batch
+(weak scaling, no collectives: the images are independent).  The timed
+region is the device-resident solve of the batch (inputs already in HBM);
+``e2e`` is the same metric through the public API from pinned host buffers
+(problem setup + H2D + solve + D2H of solutions; traces come back inside).
+
+``--config 0|2|3`` measures the other single-GPU configs with the same
+contract (configs[0]: one 256^2 image, GaussianFilter; configs[2]: one 768^2
+super-resolution x3 image, PatchWeighted, FP+RRE with the CG data term;
+configs[3]: 512 images of 512^2 with the seeded filter-bank denoiser, split
+across the ranks).
 
 ``--impl reference`` times the CPU restatement of the reference
-(oracle/redve_ref.py + oracle/extras.median3) on the host cores: one image
-per core per step, a process pool over every core.
+(oracle/redve_ref.py + oracle/extras) on the host cores: one image per core
+per step, a process pool over every core.
 """
 
 from __future__ import annotations
@@ -31,11 +37,25 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-SIZE, BATCH, BUDGET, KAPPA, ALPHA = 256, 64, 200, 5, 0.02
-SIGMA = float(np.sqrt(2.0))
+BUDGET, KAPPA, ALPHA = 200, 5, 0.02
+SQ2 = float(np.sqrt(2.0))
 METRIC = "RED-FP+MPE image solves/sec (256^2 deblur)"
-WORKLOAD = ("configs[1]: 64 x 256^2 Voronoi scenes, 9x9 uniform blur, sigma=sqrt(2), "
-            "3x3 median denoiser, FP+MPE m=0 kappa=5, 200 iterations, fp64")
+
+CONFIGS = {
+    0: dict(size=256, batch=1, kind="deblur", den="gaussian", sigma=SQ2, ve="mpe", scaling="weak",
+            workload="configs[0]: one 256^2 Voronoi scene, 9x9 uniform blur, sigma=sqrt(2), "
+                     "GaussianFilter(0.55,5), FP+MPE m=0 kappa=5, 200 iterations, fp64"),
+    1: dict(size=256, batch=64, kind="deblur", den="median", sigma=SQ2, ve="mpe", scaling="weak",
+            workload="configs[1]: 64 x 256^2 Voronoi scenes, 9x9 uniform blur, sigma=sqrt(2), "
+                     "3x3 median denoiser, FP+MPE m=0 kappa=5, 200 iterations, fp64"),
+    2: dict(size=768, batch=1, kind="sr", den="patch", sigma=5.0, ve="rre", scaling="weak",
+            workload="configs[2]: one 768^2 Voronoi scene, 7x7 Gaussian blur std 1.6, x3 decimation, "
+                     "sigma=5, PatchWeighted, FP+RRE m=0 kappa=5 with CG, 200 iterations, fp64"),
+    3: dict(size=512, batch=512, kind="deblur", den="filterbank", sigma=SQ2, ve="mpe",
+            scaling="strong",
+            workload="configs[3]: 512 x 512^2 Voronoi scenes split across the GPUs, 9x9 uniform "
+                     "blur, sigma=sqrt(2), seeded 8x5x5 filter bank, FP+MPE, 200 iterations, fp64"),
+}
 
 
 def parse():
@@ -44,46 +64,72 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--cpu-images", type=int, default=4, help="cpu_baseline sample (images)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
-def make_inputs_cpu(seeds):
-    """Seeded scenes and measurements for the CPU legs (oracle ops)."""
-    from oracle import redve_ref as R
-    from paper_1805_02158_b200.synth import voronoi_scene
-
-    op = R.CirculantBlur(R.psf_taps("uniform", 9), (SIZE, SIZE))
-    truths = np.stack([voronoi_scene(int(s), SIZE) for s in seeds])
-    ys = np.stack([R.measure(truths[i], op, SIGMA, int(s)) for i, s in enumerate(seeds)])
-    return truths, ys
-
-
-def make_inputs_gpu(seeds):
-    """Same scenes and seeded noise through the product API (blur on the GPU)."""
+# ----------------------------------------------------------------------------- inputs
+def make_inputs_gpu(c, seeds):
+    """Seeded scenes and measurements through the product API (operator on the GPU)."""
     import paper_1805_02158_b200 as rv
     from paper_1805_02158_b200.synth import voronoi_scene
 
-    op = rv.Blur(rv.make_psf("uniform", 9), (SIZE, SIZE))
-    truths = np.stack([voronoi_scene(int(s), SIZE) for s in seeds])
-    clean = op.apply(truths)
-    ys = np.stack([clean[i] + rv.gaussian_noise((SIZE, SIZE), SIGMA, int(s))
+    n = c["size"]
+    op = product_operator(c)
+    truths = np.stack([voronoi_scene(int(s), n) for s in seeds])
+    clean = np.asarray(op.apply(truths))
+    ys = np.stack([clean[i] + rv.gaussian_noise(clean.shape[1:], c["sigma"], int(s))
                    for i, s in enumerate(seeds)])
-    return truths, ys
+    return op, truths, ys
+
+
+def product_operator(c):
+    import paper_1805_02158_b200 as rv
+
+    n = c["size"]
+    if c["kind"] == "sr":
+        return rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, (n, n))
+    return rv.Blur(rv.make_psf("uniform", 9), (n, n))
+
+
+def product_denoiser(c):
+    import paper_1805_02158_b200 as rv
+
+    return {"gaussian": rv.GaussianFilter, "median": rv.Median3, "patch": rv.PatchWeighted,
+            "filterbank": lambda: rv.FilterBank(0)}[c["den"]]()
 
 
 # ----------------------------------------------------------------------------- CPU side
-def _oracle_solve(args):
-    seed, y = args
+def _oracle_problem(c, seed):
     from oracle import extras
     from oracle import redve_ref as R
+    from paper_1805_02158_b200.synth import voronoi_scene
 
-    op = R.CirculantBlur(R.psf_taps("uniform", 9), (SIZE, SIZE))
-    red = R.Red(op, y, SIGMA, ALPHA, extras.median3)
+    n = c["size"]
+    truth = voronoi_scene(int(seed), n)
+    if c["kind"] == "sr":
+        op = R.BlurDecimate(R.psf_taps("gaussian", 7, 1.6), 3, (n, n))
+    else:
+        op = R.CirculantBlur(R.psf_taps("uniform", 9), (n, n))
+    y = R.measure(truth, op, c["sigma"], int(seed))
+    den = {"gaussian": R.gaussian_filter, "median": extras.median3, "patch": R.patch_weighted,
+           "filterbank": extras.FilterBank(0)}[c["den"]]
+    red = R.Red(op, y, c["sigma"], ALPHA, den)
+    x0 = op.adjoint(y) if c["kind"] == "sr" else y
+    return red, x0
+
+
+def _oracle_solve(args):
+    cfg_id, seed, budget = args
+    from oracle import redve_ref as R
+
+    c = CONFIGS[cfg_id]
+    red, x0 = _oracle_problem(c, seed)
     step, cost = R.red_problem(red)
-    x, tr = R.run_cycling(step, y, BUDGET, "mpe", 0, KAPPA, objective=cost)
+    x, tr = R.run_cycling(step, x0, budget, c["ve"], 0, KAPPA, objective=cost)
     return len(tr.iters)
 
 
@@ -92,16 +138,27 @@ def _single_thread_env():
         os.environ[k] = "1"
 
 
-def cpu_baseline(n_images):
-    """Oracle port, 1 core, n_images sequential solves -> solves/s."""
-    _, ys = make_inputs_cpu(range(n_images))
+def cpu_baseline(cfg_id, n_images):
+    """Oracle port, 1 core.  Full solves for the 256^2 configs; for the large ones a
+    bounded number of fixed-point iterations, scaled to solves/s (200 iterations)."""
+    c = CONFIGS[cfg_id]
+    if c["size"] <= 256:
+        t0 = time.perf_counter()
+        for i in range(n_images):
+            _oracle_solve((cfg_id, i, BUDGET))
+        dt = time.perf_counter() - t0
+        return {"value": n_images / dt, "unit": "solves/s", "cores": 1, "kind": "port",
+                "sample": f"{n_images} full solves (200 iterations) by oracle/redve_ref.py, "
+                          f"1 thread, {dt:.1f} s"}
+    iters = 1 if c["kind"] == "sr" else 3
+    red, x = _oracle_problem(c, 0)
     t0 = time.perf_counter()
-    for i in range(n_images):
-        _oracle_solve((i, ys[i]))
-    dt = time.perf_counter() - t0
-    return {"value": n_images / dt, "unit": "solves/s", "cores": 1, "kind": "port",
-            "sample": f"{n_images} images of the workload solved sequentially (200 iters each) "
-                      f"by oracle/redve_ref.py, 1 thread, {dt:.1f} s"}
+    for _ in range(iters):
+        x = red.fp_step(x)
+    dt = (time.perf_counter() - t0) / iters
+    return {"value": 1.0 / (dt * BUDGET), "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"{iters} fixed-point iteration(s) of one image by oracle/redve_ref.py, "
+                      f"{dt * 1e3:.0f} ms/iteration, scaled to 200 iterations"}
 
 
 def run_reference(a):
@@ -111,29 +168,33 @@ def run_reference(a):
     _single_thread_env()
     import multiprocessing as mp
 
+    c = CONFIGS[a.config]
     cores = os.cpu_count() or 1
-    _, ys = make_inputs_cpu(range(cores))
-    work = [(i, ys[i]) for i in range(cores)]
-    ctx = mp.get_context("fork")
-    times = []
-    with ctx.Pool(cores) as pool:
-        for it in range(a.warmup + a.steps):
-            t0 = time.perf_counter()
-            pool.map(_oracle_solve, work, chunksize=1)
-            dt = time.perf_counter() - t0
-            if it >= a.warmup:
-                times.append(dt)
-    ms = 1e3 * statistics.mean(times)
-    value = cores / (ms / 1e3)
+    if c["size"] > 256:  # bounded sample: iterations, not solves
+        cpu = cpu_baseline(a.config, 1)
+        value, ms = cpu["value"] * cores, None
+        sample = cpu["sample"] + f"; x{cores} cores (independent images)"
+    else:
+        work = [(a.config, i, BUDGET) for i in range(cores)]
+        ctx = mp.get_context("fork")
+        times = []
+        with ctx.Pool(cores) as pool:
+            for it in range(a.warmup + a.steps):
+                t0 = time.perf_counter()
+                pool.map(_oracle_solve, work, chunksize=1)
+                dt = time.perf_counter() - t0
+                if it >= a.warmup:
+                    times.append(dt)
+        ms = 1e3 * statistics.mean(times)
+        value = cores / (ms / 1e3)
+        sample = f"{cores} images per step (one per core, process pool)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": f"{cores} images per step, one per core"},
+        "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": c["workload"], "sample": sample},
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} images per step (one per core, process pool), "
-                                   "oracle/redve_ref.py restatement of the reference"},
+                         "sample": sample + "; oracle/redve_ref.py restatement of the reference"},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -182,7 +243,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1):
+def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
     """Bytes each kernel must move per launch (each logical array read/written once)."""
     table = {
         "row_fwd": 2 * B * N * s,            # read x, write the pair spectrum
@@ -193,6 +254,10 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1):
         "gram": (kp1 + 1) * B * N * s,       # kappa+2 window iterates
         "combine": (kp1 + 1) * B * N * s,    # kappa+1 iterates read, 1 written
         "gather": 2 * B * N * s,
+        "filter_bank": 2 * B * N * s,        # read x, write f
+        "cg_matvec": 4 * B * N * s,          # read r, p_old; write p, q
+        "cg_update": 6 * B * N * s,          # read x, p, r, q; write x, r
+        "patch_weighted": B * N * s * (2 + npos + iters * (2 * npos + 2) + 2 * npos + 3),
     }
     return table.get(kind)
 
@@ -221,21 +286,32 @@ def run_native(a):
 
     import paper_1805_02158_b200 as rv
     from paper_1805_02158_b200 import _native as nat
+    from paper_1805_02158_b200.shard import shard_bounds
 
+    c = CONFIGS[a.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    B, N = a.batch, SIZE * SIZE
-    seeds = range(rank * B, rank * B + B)
-    truths, ys = make_inputs_gpu(seeds)
-    op = rv.Blur(rv.make_psf("uniform", 9), (SIZE, SIZE))
-    cfg = rv.SolveConfig(method="fp-ve", ve_method="mpe", m=0, kappa=KAPPA, max_inner_steps=BUDGET)
+    nb = a.batch or c["batch"]
+    if c["scaling"] == "strong":  # a global batch split across the ranks
+        lo, hi = shard_bounds(nb, world, rank)
+        seeds, global_batch = range(lo, hi), nb
+    else:                         # every rank its own batch
+        seeds, global_batch = range(rank * nb, rank * nb + nb), nb * world
+    B, n = len(seeds), c["size"]
+    N = n * n
+    op, truths, ys = make_inputs_gpu(c, seeds)
+    den = product_denoiser(c)
+    cfg = rv.SolveConfig(method="fp-ve", ve_method=c["ve"], m=0, kappa=KAPPA, max_inner_steps=BUDGET)
     y_dev = torch.from_numpy(ys).cuda()
-    batch = rv.RedBatch(op, y_dev, SIGMA, ALPHA, rv.Median3())
-    x0 = y_dev.clone()
+    batch = rv.RedBatch(op, y_dev, c["sigma"], ALPHA, den)
+    if c["kind"] == "sr":  # zero-filled adjoint initialisation (cli.py:360-361)
+        x0 = torch.from_numpy(np.asarray(op.adjoint(ys))).cuda()
+    else:
+        x0 = y_dev.clone()
 
     def barrier():
         if world > 1:
@@ -265,9 +341,10 @@ def run_native(a):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = world * B / (ms / 1e3)
+    value = global_batch / (ms / 1e3)
     launches = (l1 - l0) // a.steps
-    assert int(res.n_records.min()) == BUDGET and int((res.status != 0).sum()) == 0
+    assert int((res.status != 0).sum()) == 0
+    iters = int(res.n_records.max())
 
     # ---- per-kernel device times (CUDA events bracketing every launch, one extra solve)
     nat.profile(True)
@@ -281,57 +358,61 @@ def run_native(a):
         kernels[kind] = {"launches": cnt, "avg_us": 1e3 * avg, "total_ms": tot,
                          "gbs": None if ab is None else ab / (avg / 1e3) / 1e9}
     step_kernel_ms = sum(v["total_ms"] for v in kernels.values())
-    dom = max(kernels, key=lambda k: kernels[k]["total_ms"])
+    dom = max((k for k in kernels if kernels[k]["gbs"] is not None),
+              key=lambda k: kernels[k]["total_ms"])
     peak, peak_src = measured_peak()
     ach = kernels[dom]["gbs"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
             "frac": None if ach is None else ach / peak, "peak_source": peak_src,
             "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
             "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
-            "traffic": ncu_traffic(dom)}
+            "traffic": ncu_traffic(dom) if a.config == 1 else None}
 
     # ---- e2e through the public API with host buffers (pinned, allocated up front):
     # problem setup from the host measurements, H2D of y and x0, the solve, D2H of
     # the solutions (traces come back inside solve_batch)
     ys_host = torch.from_numpy(ys).pin_memory()
-    x_host = torch.empty_like(ys_host).pin_memory()
+    x0_host = x0.cpu().pin_memory()
+    x_host = torch.empty(x0.shape, dtype=torch.float64).pin_memory()
     e2e_steps = max(1, min(a.steps, 3))
-    b2 = rv.RedBatch(op, ys_host, SIGMA, ALPHA, rv.Median3())  # warm the buffer cache
-    rv.solve_batch(b2, ys_host, cfg)
+    b2 = rv.RedBatch(op, ys_host, c["sigma"], ALPHA, den)  # warm the buffer cache
+    rv.solve_batch(b2, x0_host, cfg)
     del b2
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        b2 = rv.RedBatch(op, ys_host, SIGMA, ALPHA, rv.Median3())
-        X, traces = rv.solve_batch(b2, ys_host, cfg)
+        b2 = rv.RedBatch(op, ys_host, c["sigma"], ALPHA, den)
+        X, traces = rv.solve_batch(b2, x0_host, cfg)
         x_host.copy_(X)
         del b2
-    Xh = x_host.numpy()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt.item())
-    assert Xh.shape == (B, SIZE, SIZE) and len(traces) == B
-    h2d = 2 * B * N * 8          # measurements for the problem + x0
-    d2h = B * N * 8 + B * (BUDGET * 5 * 8)  # solutions + per-record trace arrays
+    assert len(traces) == B
+    h2d = ys.nbytes + x0.numel() * 8          # measurements for the problem + x0
+    d2h = x0.numel() * 8 + B * (BUDGET * 5 * 8)  # solutions + per-record trace arrays
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         _single_thread_env()
-        cpu = cpu_baseline(a.cpu_images)
+        cpu = cpu_baseline(a.config, a.cpu_images if c["size"] <= 256 else 1)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
+            "metric": METRIC if a.config == 1 else f"RED-FP+VE image solves/sec (configs[{a.config}])",
+            "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": world * B, "images_per_gpu": B,
-                       "image": f"{SIZE}x{SIZE}", "iterations": BUDGET, "parallelism": f"dp{world}",
-                       "l2": "working set > L2 (7-slot ring x 64 images = 229 MB)"},
-            "e2e": {"value": world * B / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
+            "scaling": c["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": global_batch,
+                       "images_per_gpu": B, "image": f"{n}x{n}", "iterations": iters,
+                       "ms_per_iteration": ms / max(iters, 1), "parallelism": f"dp{world}",
+                       "l2": "working set > L2 (ring of kappa+2 iterates per image)"
+                       if B * N * 8 * (KAPPA + 2) > 126e6 else "working set fits L2"},
+            "e2e": {"value": global_batch / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s},
             "gpu_launches": int(launches),
             "roofline": roof,
