@@ -187,6 +187,32 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
 int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* window,
                       int method, double rank_tolerance, double* out, redve_ve_result* res);
 
+/* ---- slab primitives: spatially partitioned solve (configs[4]) ------------ */
+/* Every rank holds rows [row0, row0 + Hext) (mod Hg) of one huge image, i.e. its
+ * slab plus halos; results on rows within reach of the buffer edge are not
+ * valid.  Partial sums are returned to the host for the caller's allreduce. */
+/* (H^T H / sigma^2 + alpha I) w on the extended slab, measurement lattice by
+ * global row (objective.py:97-98 on a slab) */
+int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double sigma,
+                           double alpha, int Hext, int W, int row0, int Hg, const double* w,
+                           double* out);
+/* deterministic partial reductions (HOST out) and an in-place update */
+int redve_vec_dot(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
+int redve_vec_dist2(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
+int redve_vec_axpby(redve_ctx* ctx, int64_t n, double a, const double* x, double b, double* y);
+/* sum over interior rows [halo, halo + rows) of ((H x) - y_up)^2 at lattice points */
+int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, int W, int row0,
+                      int Hg, int halo, int rows, const double* x_ext, const double* yup_ext,
+                      double* out);
+/* window Gram of differences (HOST G, (rows-1)^2), decision (host), recombination */
+int redve_window_gram(redve_ctx* ctx, int rows, int64_t n, const double* window, double* G);
+int redve_ve_decide(redve_ctx* ctx, int kp1, const double* G, int method, double rank_tol,
+                    redve_ve_result* res, double* xi, int* needs_mgs);
+int redve_ve_decide_r(redve_ctx* ctx, int kp1, const double* R, int rank, int method,
+                      redve_ve_result* res, double* xi);
+int redve_window_combine(redve_ctx* ctx, int rows, int64_t n, const double* window, int ke,
+                         const double* xi, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -97,6 +97,22 @@ SYMBOLS = {
     "redve_cost": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _dp, _dp, _dp, _dp]),
     "redve_solve": (C.c_int, [C.c_void_p, C.POINTER(SolveConfigC), C.c_void_p, C.c_void_p,
                               C.POINTER(TraceC)]),
+    "redve_sr_normal_matvec": (C.c_int, [C.c_void_p, C.POINTER(OperatorDesc), C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                         C.c_void_p]),
+    "redve_vec_dot": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, _dp]),
+    "redve_vec_dist2": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, _dp]),
+    "redve_vec_axpby": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_double,
+                                  C.c_void_p]),
+    "redve_sr_fidelity": (C.c_int, [C.c_void_p, C.POINTER(OperatorDesc), C.c_int, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, _dp]),
+    "redve_window_gram": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, _dp]),
+    "redve_ve_decide": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int, C.c_double,
+                                  C.POINTER(VeResultC), _dp, C.POINTER(C.c_int)]),
+    "redve_ve_decide_r": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int,
+                                    C.POINTER(VeResultC), _dp]),
+    "redve_window_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_int, _dp,
+                                       C.c_void_p]),
     "redve_extrapolate": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_int,
                                     C.c_double, C.c_void_p, C.POINTER(VeResultC)]),
 }

@@ -15,6 +15,7 @@
 #include "../../include/redve_b200.h"
 #include "kernels.cuh"
 #include "rd.cuh"
+#include "slab.cuh"
 #include "sr.cuh"
 
 using namespace redve;
@@ -379,6 +380,7 @@ static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const do
   a.taps = p->htaps.as<double>();
   a.inv_sigma2 = 1.0 / (p->sigma * p->sigma); a.alpha = p->alpha;
   a.rtol = 1e-6; a.abort = 1e-4; a.maxiter = 200; a.it = 0;  // objective.py:35-37
+  a.row0 = 0; a.Hg = 0;
   a.xin = xin; a.xout = xout;
   a.hty = p->hty.as<double>(); a.f = f_ext ? f_ext : p->fbuf.as<double>();
   a.r = p->cr.as<double>(); a.p = p->cp.as<double>(); a.q = p->cq.as<double>();
@@ -1301,6 +1303,145 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
       }
     }
   }
+  return REDVE_OK;
+}
+
+// ------------------------------------------------------------------ slab primitives
+// (spatially partitioned solve, BASELINE.json configs[4]; the partial sums are
+// combined across ranks by the caller's allreduce)
+static int slab_scratch(redve_ctx* ctx, size_t bytes) {
+  CK(ctx->scratch_b.ensure(bytes));
+  return REDVE_OK;
+}
+
+int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double sigma,
+                           double alpha, int Hext, int W, int row0, int Hg, const double* w,
+                           double* out) {
+  if (op->kind != REDVE_OP_BLUR_DOWNSAMPLE || op->factor < 1 || !is_odd_pos(op->ksize))
+    return fail(ctx, REDVE_E_VALUE, "normal matvec needs a BlurDownsample operator");
+  if (!(sigma > 0) || !(alpha > 0)) return fail(ctx, REDVE_E_VALUE, "sigma, alpha must be > 0");
+  int rc = upload_taps(ctx, op);
+  if (rc) return rc;
+  CK(ctx->ve_state.ensure(sizeof(CgState) + sizeof(ImgState)));
+  CgArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = 1; a.H = Hext; a.W = W; a.factor = op->factor; a.k = op->ksize;
+  a.taps = ctx->scratch_taps.as<double>();
+  a.inv_sigma2 = 1.0 / (sigma * sigma); a.alpha = alpha;
+  a.row0 = row0; a.Hg = Hg;
+  a.xin = plain(w, (long long)Hext * W);
+  a.q = out;
+  a.cg = ctx->ve_state.as<CgState>();
+  a.st = reinterpret_cast<ImgState*>(ctx->ve_state.as<char>() + sizeof(CgState));
+  RUN(ctx, "normal_matvec", launch_normal_matvec(a, ctx->stream));
+  CKL();
+  return REDVE_OK;
+}
+
+static int vec_reduce(redve_ctx* ctx, int op, int64_t n, const double* x, const double* y,
+                      double* out) {
+  int rc = slab_scratch(ctx, sizeof(double) * 300);
+  if (rc) return rc;
+  double* part = ctx->scratch_b.as<double>();
+  RUN(ctx, "vec_reduce", launch_vec_reduce(op, n, x, y, part, part + 298, ctx->stream));
+  CKL();
+  CK(cudaMemcpyAsync(out, part + 298, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+int redve_vec_dot(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out) {
+  return vec_reduce(ctx, 0, n, x, y, out);
+}
+int redve_vec_dist2(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out) {
+  return vec_reduce(ctx, 1, n, x, y, out);
+}
+int redve_vec_axpby(redve_ctx* ctx, int64_t n, double a, const double* x, double b, double* y) {
+  RUN(ctx, "vec_axpby", launch_vec_axpby(n, a, x, b, y, ctx->stream));
+  CKL();
+  return REDVE_OK;
+}
+
+int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, int W, int row0,
+                      int Hg, int halo, int rows, const double* x_ext, const double* yup_ext,
+                      double* out) {
+  int rc = upload_taps(ctx, op);
+  if (rc) return rc;
+  if ((rc = slab_scratch(ctx, sizeof(double) * 300))) return rc;
+  double* part = ctx->scratch_b.as<double>();
+  const int f = op->kind == REDVE_OP_BLUR ? 1 : op->factor;
+  RUN(ctx, "fidelity", launch_fidelity(Hext, W, row0, Hg, halo, rows, f,
+                                       ctx->scratch_taps.as<double>(), op->ksize, x_ext, yup_ext,
+                                       part, part + 298, ctx->stream));
+  CKL();
+  CK(cudaMemcpyAsync(out, part + 298, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+
+int redve_window_gram(redve_ctx* ctx, int rows, int64_t n, const double* window, double* G) {
+  if (rows < 3 || rows - 1 > MAXKP1) return fail(ctx, REDVE_E_VALUE, "window rows out of range");
+  const int kp1 = rows - 1, ng = kp1 * (kp1 + 1) / 2;
+  int rc = slab_scratch(ctx, sizeof(double) * (296 * ng + kp1 * kp1 + 16));
+  if (rc) return rc;
+  double* part = ctx->scratch_b.as<double>();
+  double* Gd = part + 296 * ng;
+  RUN(ctx, "window_gram", launch_window_gram(rows, n, window, part, Gd, ctx->stream));
+  CKL();
+  CK(cudaMemcpyAsync(G, Gd, sizeof(double) * kp1 * kp1, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return REDVE_OK;
+}
+
+static void fill_result(const VeOut& o, redve_ve_result* res, double* xi) {
+  memset(res, 0, sizeof(*res));
+  res->converged = o.mode == VE_CONVERGED;
+  res->extrapolated = o.mode == VE_EXTRAPOLATE;
+  if (o.mode == VE_EXTRAPOLATE) {
+    res->kappa_used = o.k_used;
+    res->method = o.method;
+    res->fallback = o.fallback;
+    res->stability_sum = o.stab;
+    for (int i = 0; i <= o.k_used && i < 12; ++i) {
+      res->gamma[i] = o.gamma[i];
+      res->c[i] = o.c[i];
+      if (i < o.k_used) xi[i] = o.xi[i];
+    }
+  }
+}
+
+int redve_ve_decide(redve_ctx* ctx, int kp1, const double* G, int method, double rank_tol,
+                    redve_ve_result* res, double* xi, int* needs_mgs) {
+  if (kp1 < 2 || kp1 > MAXKP1) return fail(ctx, REDVE_E_VALUE, "window order out of range");
+  VeOut o;
+  decide_from_gram(G, kp1, method, rank_tol, o);
+  *needs_mgs = o.mode == VE_MGS;
+  fill_result(o, res, xi);
+  return REDVE_OK;
+}
+
+int redve_ve_decide_r(redve_ctx* ctx, int kp1, const double* R, int rank, int method,
+                      redve_ve_result* res, double* xi) {
+  if (kp1 < 2 || kp1 > MAXKP1) return fail(ctx, REDVE_E_VALUE, "window order out of range");
+  double Rm[MAXKP1][MAXKP1];
+  for (int i = 0; i < kp1; ++i)
+    for (int j = 0; j < kp1; ++j) Rm[i][j] = R[i * kp1 + j];
+  VeOut o;
+  decide_from_r(Rm, kp1, rank, method, o);
+  fill_result(o, res, xi);
+  return REDVE_OK;
+}
+
+int redve_window_combine(redve_ctx* ctx, int rows, int64_t n, const double* window, int ke,
+                         const double* xi, double* out) {
+  if (ke < 1 || ke > rows - 2) return fail(ctx, REDVE_E_VALUE, "bad extrapolation order");
+  int rc = slab_scratch(ctx, sizeof(double) * MAXKP1);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(ctx->scratch_b.p, xi, sizeof(double) * ke, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  RUN(ctx, "window_combine",
+      launch_window_combine(n, window, ke, ctx->scratch_b.as<double>(), out, ctx->stream));
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
   return REDVE_OK;
 }
 

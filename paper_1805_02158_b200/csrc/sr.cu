@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
     if (!takes_step(a.st[b], a.phase)) return;
   } else if (MODE == CG_ITER) {
     if (!cs.active) return;
-  } else {  // CG_RESID
+  } else if (MODE == CG_RESID) {
     if (!takes_step(a.st[b], a.phase) || !cs.need_resid) return;
   }
   const int H = a.H, W = a.W, s = a.factor, k = a.k, r = k / 2;
@@ -240,8 +240,11 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
   for (int idx = threadIdx.x; idx < HZ * WZ; idx += blockDim.x) {
     const int zi = idx / WZ, zj = idx - zi * WZ;
     const int gu = wrap(i0 - r + zi, H), gv = wrap(j0 - r + zj, W);
+    // measurement lattice by GLOBAL row (a slab of a spatially split image
+    // starts at global row a.row0 of an a.Hg-row image)
+    const int gg = (a.Hg > 0) ? (int)(((long long)a.row0 + gu) % a.Hg) : gu;
     double z = 0.0;
-    if ((gu % s) == 0 && (gv % s) == 0) {
+    if ((gg % s) == 0 && (gv % s) == 0) {
       for (int ta = 0; ta < k; ++ta)
         for (int tb = 0; tb < k; ++tb)
           z = fma(taps[ta * k + tb], ws[(zi + r - (ta - r)) * WX + (zj + r - (tb - r))], z);
@@ -262,6 +265,10 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
     const double wv = ws[(oi + 2 * r) * WX + (oj + 2 * r)];
     const double aw = fma(ht, inv_s2, a.alpha * wv);
     const long long o = (long long)b * N + (long long)gi * W + gj;
+    if (MODE == CG_PLAIN) {
+      a.q[o] = aw;
+      continue;
+    }
     if (MODE == CG_ITER) {
       a.p[o] = wv;
       a.q[o] = aw;
@@ -277,6 +284,7 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
       acc[1] = fma(res, res, acc[1]);
     }
   }
+  if (MODE == CG_PLAIN) return;
   block_sum<2>(acc, red);
   const int nblk = gridDim.x * gridDim.y;
   const int blk = blockIdx.y * gridDim.x + blockIdx.x;
@@ -390,6 +398,7 @@ int cg_update_blocks(long long N) {
 void launch_cg_init(const CgArgs& a, cudaStream_t s) { matvec_t<CG_INIT>(a, s); }
 void launch_cg_iter(const CgArgs& a, cudaStream_t s) { matvec_t<CG_ITER>(a, s); }
 void launch_cg_resid(const CgArgs& a, cudaStream_t s) { matvec_t<CG_RESID>(a, s); }
+void launch_normal_matvec(const CgArgs& a, cudaStream_t s) { matvec_t<CG_PLAIN>(a, s); }
 void launch_cg_update(const CgArgs& a, cudaStream_t s) {
   k_cg_update<<<dim3(cg_update_blocks((long long)a.H * a.W), a.B), 256, 0, s>>>(a);
 }

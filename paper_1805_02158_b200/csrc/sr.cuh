@@ -19,7 +19,7 @@ struct PwArgs {
   int phase;
 };
 
-enum CgMode : int { CG_INIT = 0, CG_ITER = 1, CG_RESID = 2 };
+enum CgMode : int { CG_INIT = 0, CG_ITER = 1, CG_RESID = 2, CG_PLAIN = 3 };
 
 struct CgState {
   double rho, beta, alpha, atol, bn2;
@@ -31,6 +31,7 @@ struct CgArgs {
   const double* taps;  // device k*k
   double inv_sigma2, alpha, rtol, abort;
   int maxiter, it;
+  int row0, Hg;        // global row of local row 0 / global height (0: the buffer is the image)
   View xin;            // CG_INIT: x_k ; CG_RESID: the solution
   View xout;           // the solution being built (warm-started copy of x_k)
   const double* hty;   // [B][N] H^T y / sigma^2
@@ -63,6 +64,7 @@ int cg_update_blocks(long long N);
 void launch_cg_init(const CgArgs& a, cudaStream_t s);
 void launch_cg_iter(const CgArgs& a, cudaStream_t s);
 void launch_cg_resid(const CgArgs& a, cudaStream_t s);
+void launch_normal_matvec(const CgArgs& a, cudaStream_t s);  // q = A w, every row
 void launch_cg_update(const CgArgs& a, cudaStream_t s);
 void launch_cg_zero_b(const CgArgs& a, cudaStream_t s);
 void launch_step_record(const RecordArgs& a, int B, cudaStream_t s);

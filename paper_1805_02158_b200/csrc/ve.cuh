@@ -26,7 +26,7 @@ namespace redve {
 enum VeMethod : int { M_MPE = 0, M_RRE = 1, M_SVDMPE = 2 };
 
 // Solve R[:n,:n] x = b (upper triangular, back substitution).
-__device__ inline void tri_upper_solve(const double (*R)[MAXKP1], int n, double* x) {
+__host__ __device__ inline void tri_upper_solve(const double (*R)[MAXKP1], int n, double* x) {
   for (int i = n - 1; i >= 0; --i) {
     double s = x[i];
     for (int j = i + 1; j < n; ++j) s -= R[i][j] * x[j];
@@ -34,7 +34,7 @@ __device__ inline void tri_upper_solve(const double (*R)[MAXKP1], int n, double*
   }
 }
 // Solve R[:n,:n]^T x = b (forward substitution).
-__device__ inline void tri_upper_t_solve(const double (*R)[MAXKP1], int n, double* x) {
+__host__ __device__ inline void tri_upper_t_solve(const double (*R)[MAXKP1], int n, double* x) {
   for (int i = 0; i < n; ++i) {
     double s = x[i];
     for (int j = 0; j < i; ++j) s -= R[j][i] * x[j];
@@ -43,7 +43,7 @@ __device__ inline void tri_upper_t_solve(const double (*R)[MAXKP1], int n, doubl
 }
 
 // Order-e annihilating (MPE-form) weights; false if the sum vanished.
-__device__ inline bool annihilating(const double (*R)[MAXKP1], int e, double* c) {
+__host__ __device__ inline bool annihilating(const double (*R)[MAXKP1], int e, double* c) {
   for (int i = 0; i < e; ++i) c[i] = -R[i][e];
   tri_upper_solve(R, e, c);
   c[e] = 1.0;
@@ -55,14 +55,14 @@ __device__ inline bool annihilating(const double (*R)[MAXKP1], int e, double* c)
   return !(fabs(s) < 1e-12 * a || !isfinite(s));
 }
 
-__device__ inline void rre_weights(const double (*R)[MAXKP1], int n, double* d) {
+__host__ __device__ inline void rre_weights(const double (*R)[MAXKP1], int n, double* d) {
   for (int i = 0; i < n; ++i) d[i] = 1.0;
   tri_upper_t_solve(R, n, d);
   tri_upper_solve(R, n, d);
 }
 
 // Right singular vector of the smallest singular value (one-sided Jacobi).
-__device__ inline bool svd_min_right(const double (*R)[MAXKP1], int n, double* vout) {
+__host__ __device__ inline bool svd_min_right(const double (*R)[MAXKP1], int n, double* vout) {
   double A[MAXKP1][MAXKP1], V[MAXKP1][MAXKP1];
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) {
@@ -123,7 +123,7 @@ struct VeOut {
 
 // Decide from R (n = kappa+1 columns, rank e known).  Shared by the Gram and
 // the MGS routes.
-__device__ inline void decide_from_r(const double (*R)[MAXKP1], int n, int e, int method,
+__host__ __device__ inline void decide_from_r(const double (*R)[MAXKP1], int n, int e, int method,
                                      VeOut& o) {
   const int kappa = n - 1;
   double c[MAXKP1];
@@ -173,7 +173,7 @@ __device__ inline void decide_from_r(const double (*R)[MAXKP1], int n, int e, in
 }
 
 // Gram route.  G is the (kappa+1)^2 symmetric Gram of the differences.
-__device__ inline void decide_from_gram(const double* G, int n, int method, double rank_tol,
+__host__ __device__ inline void decide_from_gram(const double* G, int n, int method, double rank_tol,
                                         VeOut& o) {
   double R[MAXKP1][MAXKP1];
   for (int i = 0; i < n; ++i)

@@ -1,0 +1,521 @@
+"""Spatially partitioned super-resolution solve (BASELINE.json configs[4]).
+
+One huge image is split into row slabs, one per rank (one process per GPU).
+Every rank keeps its slab plus ``halo`` rows on each side (periodic ring of
+neighbours: the last slab's bottom halo is the first slab's top rows, the
+reference's all-periodic boundary, imaging.py:8-9).  Per fixed-point step:
+
+* one halo exchange of x (reach of the denoiser and of the normal operator);
+* the denoiser on the extended slab (its result is exact on the interior
+  rows because the halo covers the denoiser's reach);
+* conjugate gradients with scipy's semantics (iterative.py:311-430) on the
+  interior, the normal operator applied to the extended search direction
+  after a halo exchange of p, every inner product allreduced;
+* the step norm, cost terms and the VE Gram allreduced, so every rank takes
+  the same decisions (termination, cadence, best iterate, extrapolation).
+
+The algebra runs in libredve_b200 slab primitives (``NativeSlabOps``); the
+collectives go through ``torch.distributed`` (NCCL on GPUs, gloo on CPU).
+SURVEY.md section 8e.  Driver semantics follow solvers.py:206-385.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+
+import numpy as np
+
+from . import _native as nat
+from .errors import CgNoConvergence, NonFiniteIterate
+from .extrapolation import METHODS
+from .shard import shard_bounds
+from .solvers import IterationTrace, TraceRecord
+from . import extrapolation as ve
+
+CG_RTOL, CG_MAXITER, CG_ABORT = 1e-6, 200, 1e-4  # objective.py:35-37
+DENSE_LOG_LIMIT = 128 * 128
+
+
+# ----------------------------------------------------------------------------- layout
+class SlabLayout:
+    """Row slab of rank ``rank``: HR rows [start, stop), LR-aligned boundaries."""
+
+    def __init__(self, H: int, W: int, factor: int, world: int, rank: int, halo: int):
+        n_lr = -(-H // factor)
+        lo, hi = shard_bounds(n_lr, world, rank)
+        self.start = lo * factor
+        self.stop = H if rank == world - 1 else hi * factor
+        self.rows = self.stop - self.start
+        self.H, self.W, self.factor, self.halo = H, W, factor, halo
+        if self.rows < halo:
+            raise ValueError(f"slab of {self.rows} rows is thinner than the halo ({halo})")
+        self.Hext = self.rows + 2 * halo
+        self.row0 = (self.start - halo) % H  # global row of extended row 0
+
+    def ext_rows(self):
+        return [(self.row0 + u) % self.H for u in range(self.Hext)]
+
+
+def denoiser_reach(denoiser) -> int:
+    name = type(denoiser).__name__
+    if name == "PatchWeighted":
+        pr, sr, it = denoiser.patch_radius, denoiser.search_radius, denoiser.balance_iters
+        return pr + 2 * sr + sr * (it + 1)
+    if name == "Median3":
+        return 1
+    if name == "GaussianFilter":
+        return denoiser.psf.radius
+    if name == "FilterBank":
+        return 2 * (denoiser.size // 2)
+    if name == "Identity":
+        return 0
+    raise TypeError(f"no reach known for denoiser {name}")
+
+
+# ----------------------------------------------------------------------------- comm
+class TorchComm:
+    """Halo exchange + scalar allreduce over torch.distributed (or a single rank)."""
+
+    def __init__(self, group=None, device="cpu"):
+        import torch.distributed as dist
+
+        self.dist = dist if (dist.is_available() and dist.is_initialized()) else None
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.group = group
+        self.device = device  # where collective buffers live ("cpu" for gloo)
+
+    def allreduce(self, vals):
+        import torch
+
+        if self.world == 1:
+            return [float(v) for v in vals]
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, group=self.group)
+        return [float(v) for v in t.cpu().tolist()]
+
+    def exchange(self, ext, halo: int, rows: int):
+        """Fill ext[:halo] / ext[halo+rows:] (row-major [Hext, W] tensor) from the ring."""
+        import torch
+
+        if halo == 0:
+            return
+        top_int = ext[halo: 2 * halo]              # my first interior rows
+        bot_int = ext[rows: rows + halo]            # my last interior rows
+        if self.world == 1:
+            ext[:halo].copy_(bot_int)
+            ext[halo + rows:].copy_(top_int)
+            return
+        prev = (self.rank - 1) % self.world
+        nxt = (self.rank + 1) % self.world
+        dev = self.device
+        send_bot = bot_int.contiguous().to(dev)
+        send_top = top_int.contiguous().to(dev)
+        recv_top = torch.empty_like(send_top)
+        recv_bot = torch.empty_like(send_bot)
+        P2P = self.dist.P2POp
+        ops = [P2P(self.dist.isend, send_bot, nxt, self.group),
+               P2P(self.dist.isend, send_top, prev, self.group),
+               P2P(self.dist.irecv, recv_top, prev, self.group),
+               P2P(self.dist.irecv, recv_bot, nxt, self.group)]
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+        ext[:halo].copy_(recv_top)
+        ext[halo + rows:].copy_(recv_bot)
+
+
+# ----------------------------------------------------------------------------- local ops
+class NativeSlabOps:
+    """Slab algebra in libredve_b200 (device tensors)."""
+
+    def __init__(self, forward, sigma, alpha, denoiser):
+        import torch
+
+        self.torch = torch
+        self.forward, self.sigma, self.alpha, self.denoiser = forward, sigma, alpha, denoiser
+        self.lib = nat.library()
+        self.ctx = nat.context()
+        d = nat.OperatorDesc()
+        d.kind = nat.OP_BLUR_DOWNSAMPLE
+        d.ksize = forward.psf.size
+        d.taps = nat.hptr(forward.psf.taps)
+        d.factor = forward.factor
+        self.op = d
+        b = nat.OperatorDesc()
+        b.kind = nat.OP_BLUR
+        b.ksize = forward.psf.size
+        b.taps = nat.hptr(forward.psf.taps)
+        b.factor = 1
+        self.blur = b
+
+    def tensor(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a), dtype=self.torch.float64).cuda()
+
+    def zeros(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.float64, device="cuda")
+
+    def host(self, t):
+        return t.detach().cpu().numpy()
+
+    def copy(self, t):
+        return t.clone()
+
+    def denoise(self, x_ext):
+        return self.denoiser(x_ext)
+
+    def correlate(self, z_ext, scale):
+        out = self.zeros(z_ext.shape)
+        nat.check(self.lib.redve_operator_adjoint(self.ctx, C.byref(self.blur), 1, z_ext.shape[0],
+                                                  z_ext.shape[1], nat.dptr(z_ext), nat.dptr(out)),
+                  self.ctx)
+        self.axpby(0.0, out, scale, out)
+        return out
+
+    def normal_matvec(self, w_ext, row0, Hg):
+        out = self.zeros(w_ext.shape)
+        nat.check(self.lib.redve_sr_normal_matvec(self.ctx, C.byref(self.op), self.sigma, self.alpha,
+                                                  w_ext.shape[0], w_ext.shape[1], row0, Hg,
+                                                  nat.dptr(w_ext), nat.dptr(out)), self.ctx)
+        return out
+
+    def _red(self, fn, x, y):
+        v = C.c_double()
+        nat.check(fn(self.ctx, x.numel(), nat.dptr(x), nat.dptr(y), C.byref(v)), self.ctx)
+        return v.value
+
+    def dot(self, x, y):
+        return self._red(self.lib.redve_vec_dot, x.contiguous(), y.contiguous())
+
+    def dist2(self, x, y):
+        return self._red(self.lib.redve_vec_dist2, x.contiguous(), y.contiguous())
+
+    def axpby(self, a, x, b, y):
+        nat.check(self.lib.redve_vec_axpby(self.ctx, y.numel(), float(a), nat.dptr(x), float(b),
+                                           nat.dptr(y)), self.ctx)
+
+    def fidelity(self, x_ext, yup_ext, row0, Hg, halo, rows):
+        v = C.c_double()
+        nat.check(self.lib.redve_sr_fidelity(self.ctx, C.byref(self.op), x_ext.shape[0],
+                                             x_ext.shape[1], row0, Hg, halo, rows,
+                                             nat.dptr(x_ext), nat.dptr(yup_ext), C.byref(v)),
+                  self.ctx)
+        return v.value
+
+    def window_gram(self, window):
+        rows = window.shape[0]
+        G = np.zeros((rows - 1, rows - 1))
+        nat.check(self.lib.redve_window_gram(self.ctx, rows, window[0].numel(), nat.dptr(window),
+                                             nat.hptr(G)), self.ctx)
+        return G
+
+    def decide(self, G, method, rank_tol):
+        kp1 = G.shape[0]
+        res = nat.VeResultC()
+        xi = np.zeros(12)
+        need = C.c_int()
+        G = np.ascontiguousarray(G)
+        nat.check(self.lib.redve_ve_decide(self.ctx, kp1, nat.hptr(G), nat.VE_CODES[method],
+                                           rank_tol, C.byref(res), nat.hptr(xi), C.byref(need)),
+                  self.ctx)
+        return res, xi, bool(need.value)
+
+    def decide_r(self, R, rank, method):
+        kp1 = R.shape[0]
+        res = nat.VeResultC()
+        xi = np.zeros(12)
+        R = np.ascontiguousarray(R)
+        nat.check(self.lib.redve_ve_decide_r(self.ctx, kp1, nat.hptr(R), rank, nat.VE_CODES[method],
+                                             C.byref(res), nat.hptr(xi)), self.ctx)
+        return res, xi
+
+    def combine(self, window, ke, xi):
+        out = self.zeros(window.shape[1:])
+        xi = np.ascontiguousarray(xi[:ke])
+        nat.check(self.lib.redve_window_combine(self.ctx, window.shape[0], window[0].numel(),
+                                                nat.dptr(window), ke, nat.hptr(xi),
+                                                nat.dptr(out)), self.ctx)
+        return out
+
+    def stack(self, vs):
+        return self.torch.stack(vs).contiguous()
+
+
+# ----------------------------------------------------------------------------- driver
+class SpatialProblem:
+    """One SR problem split across the ranks of ``comm`` (RedObjective over slabs)."""
+
+    def __init__(self, forward, y, sigma, alpha, denoiser, comm=None, ops=None, reference=None,
+                 reach=None):
+        if sigma <= 0 or alpha <= 0:
+            raise ValueError("sigma, alpha must be > 0")
+        self.comm = comm or TorchComm()
+        self.ops = ops or NativeSlabOps(forward, sigma, alpha, denoiser)
+        H, W = forward.in_shape
+        self.H, self.W, self.s = H, W, forward.factor
+        self.sigma, self.alpha = float(sigma), float(alpha)
+        r = forward.psf.radius
+        halo = max(denoiser_reach(denoiser) if reach is None else int(reach), 2 * r)
+        self.lay = SlabLayout(H, W, self.s, self.comm.world, self.comm.rank, halo)
+        lay = self.lay
+        y = np.asarray(y, dtype=np.float64)
+        yup = np.zeros((lay.Hext, W))
+        for u, g in enumerate(lay.ext_rows()):
+            if g % self.s == 0:
+                yup[u, ::self.s] = y[g // self.s]
+        self.yup = self.ops.tensor(yup)
+        self.hty = self.ops.correlate(self.yup, 1.0 / self.sigma**2)[lay.halo: lay.halo + lay.rows]
+        self.ref = None if reference is None else self.ops.tensor(
+            np.asarray(reference, dtype=np.float64)[lay.start: lay.stop])
+        self.N = H * W
+
+    # -- helpers
+    def slab(self, x_global):
+        return self.ops.tensor(np.asarray(x_global, dtype=np.float64)[self.lay.start: self.lay.stop])
+
+    def extend(self, x):
+        lay = self.lay
+        ext = self.ops.zeros((lay.Hext, self.W))
+        ext[lay.halo: lay.halo + lay.rows].copy_(x)
+        self.comm.exchange(ext, lay.halo, lay.rows)
+        return ext
+
+    def interior(self, ext):
+        lay = self.lay
+        return ext[lay.halo: lay.halo + lay.rows]
+
+    def gdot(self, pairs):
+        return self.comm.allreduce([self.ops.dot(a, b) for a, b in pairs])
+
+    def matvec(self, p):
+        ext = self.extend(p)
+        return self.interior(self.ops.normal_matvec(ext, self.lay.row0, self.H)).contiguous()
+
+    # -- objective pieces (objective.py:78-121 on slabs)
+    def denoise(self, x):
+        return self.interior(self.ops.denoise(self.extend(x))).contiguous()
+
+    def cost_terms(self, x):
+        ext = self.extend(x)
+        f = self.interior(self.ops.denoise(ext)).contiguous()
+        fid = self.ops.fidelity(ext, self.yup, self.lay.row0, self.H, self.lay.halo, self.lay.rows)
+        vals = [fid, self.ops.dot(x, x), self.ops.dot(x, f)]
+        if self.ref is not None:
+            vals.append(self.ops.dist2(x, self.ref))
+        tot = self.comm.allreduce(vals)
+        cost = tot[0] / (2 * self.sigma**2) + self.alpha * 0.5 * (tot[1] - tot[2])
+        ps = None
+        if self.ref is not None:
+            mse = tot[3] / self.N
+            ps = math.inf if mse == 0 else (-math.inf if not np.isfinite(mse)
+                                            else 10 * math.log10(255.0**2 / mse))
+        return cost, ps
+
+    def fp_step(self, x):
+        """CG fixed-point step with scipy semantics; returns (x_new, cg_iterations)."""
+        ops = self.ops
+        f = self.denoise(x)
+        b = ops.copy(self.hty)
+        ops.axpby(self.alpha, f, 1.0, b)                 # b = hty + alpha f
+        xn = ops.copy(x)
+        q = self.matvec(xn)
+        r = ops.copy(b)
+        ops.axpby(-1.0, q, 1.0, r)                       # r = b - A x
+        bn2, rho = self.gdot([(b, b), (r, r)])
+        bn = math.sqrt(bn2)
+        if bn == 0:
+            return b, 0
+        atol = CG_RTOL * bn
+        p = None
+        rho_prev = None
+        its = 0
+        info = CG_MAXITER
+        for it in range(CG_MAXITER):
+            if math.sqrt(rho) < atol:
+                info = 0
+                break
+            if it > 0:
+                ops.axpby(1.0, r, rho / rho_prev, p)      # p = r + beta p
+            else:
+                p = ops.copy(r)
+            q = self.matvec(p)
+            (pq,) = self.gdot([(p, q)])
+            a = rho / pq
+            ops.axpby(a, p, 1.0, xn)
+            ops.axpby(-a, q, 1.0, r)
+            rho_prev = rho
+            (rho,) = self.gdot([(r, r)])
+            its += 1
+        if info != 0:  # objective.py:114-120
+            res = ops.copy(b)
+            ops.axpby(-1.0, self.matvec(xn), 1.0, res)
+            rn2, bn2b = self.gdot([(res, res), (b, b)])
+            if math.sqrt(rn2) > CG_ABORT * math.sqrt(bn2b):
+                raise CgNoConvergence(f"CG residual {math.sqrt(rn2):.3e} after {CG_MAXITER} iterations")
+        return xn, its
+
+    def gather(self, x):
+        """The full image on every rank (host numpy)."""
+        import torch
+
+        xs = self.ops.host(x)
+        if self.comm.world == 1:
+            return xs
+        dist = self.comm.dist
+        H, W = self.H, self.W
+        maxr = max(SlabLayout(H, W, self.s, self.comm.world, r, 0).rows
+                   for r in range(self.comm.world))
+        buf = torch.zeros((maxr, W), dtype=torch.float64, device=self.comm.device)
+        buf[: xs.shape[0]] = torch.from_numpy(xs).to(self.comm.device)
+        parts = [torch.empty_like(buf) for _ in range(self.comm.world)]
+        dist.all_gather(parts, buf, group=self.comm.group)
+        out = [parts[r][: SlabLayout(H, W, self.s, self.comm.world, r, 0).rows].cpu().numpy()
+               for r in range(self.comm.world)]
+        return np.concatenate(out)
+
+
+def _extrapolate(prob, window_list, method, rank_tol):
+    """extrapolate_once on a distributed window (extrapolation.py:319-386)."""
+    ops = prob.ops
+    window = ops.stack(window_list)
+    G = np.asarray(prob.comm.allreduce(ops.window_gram(window).ravel().tolist())).reshape(
+        len(window_list) - 1, len(window_list) - 1)
+    res, xi, need_mgs = ops.decide(G, method, rank_tol)
+    if need_mgs:  # exact MGS with distributed inner products (rare)
+        res, xi = _mgs_decide(prob, window_list, method, rank_tol)
+    if res.converged:
+        return "converged", window_list[0], None
+    if not res.extrapolated:
+        return "skip", window_list[-1], None
+    x = ops.combine(window, res.kappa_used, xi)
+    k = res.kappa_used
+    w = ve.ExtrapolationWeights(method=nat.VE_NAMES[res.method], c=np.array(res.c[: k + 1]),
+                                gamma=np.array(res.gamma[: k + 1]),
+                                stability_sum=float(res.stability_sum),
+                                fallback_from=method if res.fallback else None)
+    return "extrapolated", x, w
+
+
+def _mgs_decide(prob, vs, method, rank_tol):
+    ops = prob.ops
+    n = len(vs) - 1
+    R = np.zeros((n, n))
+    Q = []
+    rank = n
+    r11 = 0.0
+    for i in range(n):
+        v = ops.copy(vs[i + 1])
+        ops.axpby(-1.0, vs[i], 1.0, v)
+        for _sweep in range(2):
+            for j in range(i):
+                (c,) = prob.gdot([(Q[j], v)])
+                R[j, i] += c
+                ops.axpby(-c, Q[j], 1.0, v)
+        (nn,) = prob.gdot([(v, v)])
+        rii = math.sqrt(nn)
+        R[i, i] = rii
+        if i == 0:
+            if rii < 1e-300:
+                res = nat.VeResultC()
+                res.converged = 1
+                return res, np.zeros(12)
+            r11 = rii
+        elif rii < rank_tol * r11:
+            rank = i
+            break
+        ops.axpby(0.0, v, 1.0 / rii, v)
+        Q.append(v)
+    return ops.decide_r(R, rank, method)
+
+
+def solve_spatial(prob: SpatialProblem, x0_global, config, reference_trace=True):
+    """run_fixed_point / run_ve_cycling (solvers.py:288-298, 340-385) for one image
+    split across ranks.  Returns (x_global on every rank, IterationTrace)."""
+    method = config.method
+    if method not in ("fp", "fp-ve"):
+        raise ValueError("spatial solve supports 'fp' and 'fp-ve'")
+    if config.ve_method not in METHODS:
+        raise ValueError("unknown VE method")
+    ops = prob.ops
+    x = prob.slab(x0_global)
+    trace = IterationTrace()
+    every = 1 if prob.N <= DENSE_LOG_LIMIT else 5
+    track = method == "fp-ve"
+    best_cost, best_x = math.inf, None
+    t0 = time.perf_counter()
+    k = 0
+
+    def record(xp, xn):
+        nonlocal k, best_cost, best_x
+        k += 1
+        d2, x2 = prob.comm.allreduce([ops.dist2(xn, xp), ops.dot(xp, xp)])
+        den = math.sqrt(x2) or 1.0
+        sn = math.sqrt(d2) / den
+        cost = ps = None
+        if k % every == 0:
+            cost, ps = prob.cost_terms(xn)
+            if track and cost < best_cost:
+                best_cost, best_x = cost, ops.copy(xn)
+        trace.records.append(TraceRecord(k, cost, ps if prob.ref is not None else None, sn, None,
+                                          time.perf_counter() - t0))
+        if not (np.isfinite(d2) and np.isfinite(x2)):
+            raise NonFiniteIterate(f"iterate diverged at inner step {k}", trace)
+        if cost is not None and not np.isfinite(cost):
+            raise NonFiniteIterate(f"objective diverged at inner step {k}", trace)
+        if sn <= config.tol:
+            return "converged"
+        if k >= config.max_inner_steps:
+            return "budget"
+        return None
+
+    if not track:
+        while True:
+            xn, _ = prob.fp_step(x)
+            d = record(x, xn)
+            x = xn
+            if d is not None:
+                break
+        return prob.gather(x), trace
+
+    c0, _ = prob.cost_terms(x)
+    if np.isfinite(c0):
+        best_cost, best_x = c0, ops.copy(x)
+    clen = config.m + config.kappa + 1
+    while True:
+        xs = [x]
+        conv = False
+        for _ in range(clen):
+            xn, _ = prob.fp_step(x)
+            d = record(x, xn)
+            x = xn
+            xs.append(x)
+            if d == "converged":
+                conv = True
+                break
+            if d == "budget":
+                break
+        if conv:
+            break
+        if len(xs) == clen + 1:
+            kind, xv, w = _extrapolate(prob, xs[config.m:], config.ve_method, config.rank_tolerance)
+            if kind == "converged":
+                x = xv
+                break
+            if kind == "extrapolated":
+                (nf,) = prob.comm.allreduce([0.0 if np.isfinite(ops.dot(xv, xv)) else 1.0])
+                if nf == 0:
+                    x = xv
+                    trace.records[-1].gamma_abs_sum = w.stability_sum
+                    trace.cycle_weights.append(w)
+        if k >= config.max_inner_steps:
+            break
+    for _ in range(config.stabilization_iters):
+        xn, _ = prob.fp_step(x)
+        record(x, xn)
+        x = xn
+    if best_x is not None:
+        cf, _ = prob.cost_terms(x)
+        if not (np.isfinite(cf) and cf <= best_cost):
+            x = best_x
+    return prob.gather(x), trace
