@@ -40,6 +40,7 @@ sys.path.insert(0, REPO)
 BUDGET, KAPPA, ALPHA = 200, 5, 0.02
 SQ2 = float(np.sqrt(2.0))
 METRIC = "RED-FP+MPE image solves/sec (256^2 deblur)"
+SPATIAL_METRIC = "RED-FP+RRE fixed-point iterations/sec (configs[4], 8192^2 SR x3, one image)"
 
 CONFIGS = {
     0: dict(size=256, batch=1, kind="deblur", den="gaussian", sigma=SQ2, ve="mpe", scaling="weak",
@@ -55,7 +56,13 @@ CONFIGS = {
             scaling="strong",
             workload="configs[3]: 512 x 512^2 Voronoi scenes split across the GPUs, 9x9 uniform "
                      "blur, sigma=sqrt(2), seeded 8x5x5 filter bank, FP+MPE, 200 iterations, fp64"),
+    4: dict(size=8192, batch=1, kind="sr", den="patch", sigma=5.0, ve="rre", scaling="strong",
+            workload="configs[4]: one 8192^2 Voronoi scene (LR 2731^2), 7x7 Gaussian blur std 1.6, "
+                     "x3 decimation, sigma=5, PatchWeighted, FP+RRE m=0 kappa=5 with CG, fp64; "
+                     "row slabs across the GPUs with halo exchange + allreduced inner products; "
+                     "one step = the first 7 fixed-point iterations + 1 extrapolation"),
 }
+SPATIAL_BUDGET = 7
 
 
 def parse():
@@ -162,6 +169,21 @@ def cpu_baseline(cfg_id, n_images, iters_per_solve=BUDGET):
                       f"{dt * 1e3:.0f} ms/iteration, scaled to {iters_per_solve} iterations"}
 
 
+def cpu_baseline_spatial():
+    """configs[4] on the CPU: one oracle fixed-point iteration of the configs[2]
+    problem (768^2, same operator/denoiser/CG), scaled by the pixel ratio to
+    8192^2 (every piece is O(N) or O(N log N) per iteration)."""
+    red, x = _oracle_problem(CONFIGS[2], 0)
+    t0 = time.perf_counter()
+    red.fp_step(x)
+    dt = time.perf_counter() - t0
+    scale = (8192 / 768) ** 2
+    its_s = 1.0 / (dt * scale)
+    return {"value": its_s, "unit": "iterations/s", "cores": 1, "kind": "port",
+            "sample": f"1 fixed-point iteration of a 768^2 SR problem by oracle/redve_ref.py "
+                      f"({dt:.1f} s), scaled x{scale:.1f} by pixel count to 8192^2"}
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -171,6 +193,18 @@ def run_reference(a):
 
     c = CONFIGS[a.config]
     cores = os.cpu_count() or 1
+    if a.config == 4:  # one huge image: the CPU path is a single process
+        cpu = cpu_baseline_spatial()
+        line = {"impl": "reference", "metric": SPATIAL_METRIC, "value": cpu["value"],
+                "unit": "iterations/s", "n_gpus": a.gpus, "steps": 1, "warmup": 0,
+                "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": c["workload"], "sample": cpu["sample"]},
+                "cpu_baseline": cpu,
+                "e2e": {"value": cpu["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     if c["size"] > 256:  # bounded sample: iterations, not solves
         cpu = cpu_baseline(a.config, 1)
         value, ms = cpu["value"] * cores, None
@@ -258,7 +292,16 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
         "filter_bank": 2 * B * N * s,        # read x, write f
         "cg_matvec": 4 * B * N * s,          # read r, p_old; write p, q
         "cg_update": 6 * B * N * s,          # read x, p, r, q; write x, r
-        "patch_weighted": B * N * s * (2 + npos + iters * (2 * npos + 2) + 2 * npos + 3),
+        # raw weights: read x, write the 24 half-plane planes; each balancing sweep:
+        # read the planes + D, write D; apply: read planes, D, x, write f
+        "patch_weighted": B * N * s * (1 + npos + iters * (npos + 2) + npos + 3),
+        # slab primitives of the spatial solve (configs[4])
+        "normal_matvec": 2 * B * N * s,      # read w, write out
+        "vec_reduce": 2 * B * N * s,         # read x, y
+        "vec_axpby": 3 * B * N * s,          # read x, y; write y
+        "fidelity": B * N * s + B * N * s // 9,
+        "window_gram": (kp1 + 1) * B * N * s,
+        "window_combine": (kp1 + 1) * B * N * s,
     }
     return table.get(kind)
 
@@ -426,10 +469,141 @@ def run_native(a):
         dist.destroy_process_group()
 
 
+def run_spatial(a):
+    """configs[4]: one 8192^2 SR image split into row slabs across the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_02158_b200 as rv
+    from paper_1805_02158_b200 import _native as nat
+    from paper_1805_02158_b200.spatial import SpatialProblem, TorchComm, solve_spatial
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    c = CONFIGS[4]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = c["size"]
+    op = product_operator(c)
+    truth = voronoi_scene(0, n)
+    clean = np.asarray(op.apply(truth))
+    y = clean + rv.gaussian_noise(clean.shape, c["sigma"], 0)
+    x0 = np.asarray(op.adjoint(y))            # zero-filled adjoint initialisation
+    del clean
+    den = product_denoiser(c)
+    comm = TorchComm(device="cuda")
+    prob = SpatialProblem(op, y, c["sigma"], ALPHA, den, comm=comm, reference=truth)
+    cfg = rv.SolveConfig(method="fp-ve", ve_method="rre", m=0, kappa=KAPPA,
+                         max_inner_steps=SPATIAL_BUDGET)
+    gather = prob.gather
+    x0_slab = prob.slab(x0)                   # resident in HBM before the timed region
+
+    def one_step():
+        prob.gather = lambda x: x          # the timed step keeps the result on the device
+        try:
+            return solve_spatial(prob, x0_slab, cfg)
+        finally:
+            prob.gather = gather
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = nat.kernel_launches()
+    e0.record(stream)
+    for _ in range(a.steps):
+        _, tr = one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    l1 = nat.kernel_launches()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    iters = len(tr.records)
+    value = iters / (ms / 1e3)
+
+    nat.profile(True)
+    one_step()
+    rep = nat.profile_report()
+    nat.profile(False)
+    lay = prob.lay
+    Next = lay.Hext * n
+    kernels = {}
+    ext_kinds = ("patch_weighted", "normal_matvec", "upsample_corr")
+    for kind, (tot, cnt) in rep.items():
+        ab = algorithmic_bytes(kind, 1, Next if kind in ext_kinds else lay.rows * n)
+        avg = tot / cnt
+        kernels[kind] = {"launches": cnt, "avg_us": 1e3 * avg, "total_ms": tot,
+                         "gbs": None if ab is None else ab / (avg / 1e3) / 1e9}
+    step_kernel_ms = sum(v["total_ms"] for v in kernels.values())
+    dom = max((k for k in kernels if kernels[k]["gbs"] is not None),
+              key=lambda k: kernels[k]["total_ms"])
+    peak, peak_src = measured_peak()
+    ach = kernels[dom]["gbs"]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "peak_source": peak_src,
+            "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
+            "algorithmic_bytes_per_launch": algorithmic_bytes(
+                dom, 1, Next if dom in ext_kinds else lay.rows * n), "traffic": None}
+
+    # e2e through the public API: problem setup from the host measurements (H2D of
+    # the slab's y and x0), the solve, the gathered host image out
+    barrier()
+    t0 = time.perf_counter()
+    prob2 = SpatialProblem(op, y, c["sigma"], ALPHA, den, comm=comm, reference=truth)
+    x_host, _ = solve_spatial(prob2, x0, cfg)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s = float(tt.item())
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        _single_thread_env()
+        cpu = cpu_baseline_spatial()
+    if rank == 0:
+        line = {
+            "metric": SPATIAL_METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["workload"], "image": f"{n}x{n}", "iterations": iters,
+                       "ms_per_iteration": ms / iters, "parallelism": f"spatial{world}",
+                       "slab_rows": lay.rows, "halo_rows": lay.halo,
+                       "l2": "working set > L2 (8192^2 fp64 = 512 MiB per image)"},
+            "e2e": {"value": iters / e2e_s, "unit": "iterations/s",
+                    "h2d_bytes_per_step": (lay.Hext + 2 * lay.rows) * n * 8,
+                    "d2h_bytes_per_step": n * n * 8, "ms_per_step": 1e3 * e2e_s},
+            "gpu_launches": int((l1 - l0) // a.steps),
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == 4:
+        run_spatial(a)
     else:
         run_native(a)
 

@@ -109,6 +109,8 @@ struct redve_ctx {
   std::map<int, DevBuf*> twiddles, stage_twiddles;
   DevBuf scratch_taps, scratch_a, scratch_b, ve_ring, ve_state, ve_partials, ve_counters,
       ve_q, ve_trace;
+  std::vector<double> taps_host;  // what scratch_taps holds (skip identical re-uploads)
+  void* taps_dev = nullptr;
   ~redve_ctx() {
     for (auto& kv : twiddles) delete kv.second;
     for (auto& kv : stage_twiddles) delete kv.second;
@@ -484,6 +486,20 @@ int redve_synchronize(redve_ctx* ctx) {
   return REDVE_OK;
 }
 
+// k x k host taps into scratch_taps; identical taps already resident are not
+// re-sent (a pageable upload would serialise the stream with the host)
+static int put_taps(redve_ctx* ctx, const double* taps, int k) {
+  const size_t n = (size_t)k * k, kb = sizeof(double) * n;
+  CK(ctx->scratch_taps.ensure(kb));
+  if (ctx->taps_dev == ctx->scratch_taps.p && ctx->taps_host.size() == n &&
+      memcmp(ctx->taps_host.data(), taps, kb) == 0)
+    return REDVE_OK;
+  CK(cudaMemcpyAsync(ctx->scratch_taps.p, taps, kb, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->taps_host.assign(taps, taps + n);
+  ctx->taps_dev = ctx->scratch_taps.p;
+  return REDVE_OK;
+}
+
 // ------------------------------------------------------------------ denoise
 int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
                   const double* x, double* out) {
@@ -501,9 +517,8 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       if (!is_odd_pos(dn->ksize)) return fail(ctx, REDVE_E_VALUE, "kernel size must be odd");
       if (dn->ksize > H || dn->ksize > W)
         return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
-      size_t kb = sizeof(double) * dn->ksize * dn->ksize;
-      CK(ctx->scratch_taps.ensure(kb));
-      CK(cudaMemcpyAsync(ctx->scratch_taps.p, dn->taps, kb, cudaMemcpyHostToDevice, ctx->stream));
+      int rc = put_taps(ctx, dn->taps, dn->ksize);
+      if (rc) return rc;
       RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), dn->ksize, 0, 1.0, ctx->stream));
       CKL();
       // taps buffer is reused by the next call: keep it alive until then
@@ -603,10 +618,7 @@ static int op_check(redve_ctx* ctx, const redve_operator_desc* op, int H, int W)
 }
 
 static int upload_taps(redve_ctx* ctx, const redve_operator_desc* op) {
-  size_t kb = sizeof(double) * op->ksize * op->ksize;
-  CK(ctx->scratch_taps.ensure(kb));
-  CK(cudaMemcpyAsync(ctx->scratch_taps.p, op->taps, kb, cudaMemcpyHostToDevice, ctx->stream));
-  return REDVE_OK;
+  return put_taps(ctx, op->taps, op->ksize);
 }
 
 int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, int H, int W,
@@ -652,6 +664,8 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   if (B < 1 || H < 1 || W < 1) return fail(ctx, REDVE_E_VALUE, "bad batch shape");
   int rc = op_check(ctx, op, H, W);
   if (rc) return rc;
+  if (op->kind == REDVE_OP_BLUR_DOWNSAMPLE && op->ksize > 31)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "the fused CG normal operator takes PSFs up to 31x31");
   if (dn->kind == REDVE_DN_CONV) {
     if (!is_odd_pos(dn->ksize)) return fail(ctx, REDVE_E_VALUE, "denoiser kernel must be odd");
     if (dn->ksize > H || dn->ksize > W)
@@ -1319,6 +1333,8 @@ int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double
                            double* out) {
   if (op->kind != REDVE_OP_BLUR_DOWNSAMPLE || op->factor < 1 || !is_odd_pos(op->ksize))
     return fail(ctx, REDVE_E_VALUE, "normal matvec needs a BlurDownsample operator");
+  if (op->ksize > 31)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "the fused normal operator takes PSFs up to 31x31");
   if (!(sigma > 0) || !(alpha > 0)) return fail(ctx, REDVE_E_VALUE, "sigma, alpha must be > 0");
   int rc = upload_taps(ctx, op);
   if (rc) return rc;
@@ -1340,12 +1356,13 @@ int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double
 
 static int vec_reduce(redve_ctx* ctx, int op, int64_t n, const double* x, const double* y,
                       double* out) {
-  int rc = slab_scratch(ctx, sizeof(double) * 300);
+  int rc = slab_scratch(ctx, sizeof(double) * (SLAB_BLOCKS + 2));
   if (rc) return rc;
   double* part = ctx->scratch_b.as<double>();
-  RUN(ctx, "vec_reduce", launch_vec_reduce(op, n, x, y, part, part + 298, ctx->stream));
+  RUN(ctx, "vec_reduce",
+      launch_vec_reduce(op, n, x, y, part, part + SLAB_BLOCKS, ctx->stream));
   CKL();
-  CK(cudaMemcpyAsync(out, part + 298, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(out, part + SLAB_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return REDVE_OK;
 }
@@ -1366,14 +1383,14 @@ int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, i
                       double* out) {
   int rc = upload_taps(ctx, op);
   if (rc) return rc;
-  if ((rc = slab_scratch(ctx, sizeof(double) * 300))) return rc;
+  if ((rc = slab_scratch(ctx, sizeof(double) * (SLAB_BLOCKS + 2)))) return rc;
   double* part = ctx->scratch_b.as<double>();
   const int f = op->kind == REDVE_OP_BLUR ? 1 : op->factor;
   RUN(ctx, "fidelity", launch_fidelity(Hext, W, row0, Hg, halo, rows, f,
                                        ctx->scratch_taps.as<double>(), op->ksize, x_ext, yup_ext,
-                                       part, part + 298, ctx->stream));
+                                       part, part + SLAB_BLOCKS, ctx->stream));
   CKL();
-  CK(cudaMemcpyAsync(out, part + 298, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(out, part + SLAB_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return REDVE_OK;
 }
@@ -1381,10 +1398,10 @@ int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, i
 int redve_window_gram(redve_ctx* ctx, int rows, int64_t n, const double* window, double* G) {
   if (rows < 3 || rows - 1 > MAXKP1) return fail(ctx, REDVE_E_VALUE, "window rows out of range");
   const int kp1 = rows - 1, ng = kp1 * (kp1 + 1) / 2;
-  int rc = slab_scratch(ctx, sizeof(double) * (296 * ng + kp1 * kp1 + 16));
+  int rc = slab_scratch(ctx, sizeof(double) * (GRAM_BLOCKS * ng + kp1 * kp1 + 16));
   if (rc) return rc;
   double* part = ctx->scratch_b.as<double>();
-  double* Gd = part + 296 * ng;
+  double* Gd = part + GRAM_BLOCKS * ng;
   RUN(ctx, "window_gram", launch_window_gram(rows, n, window, part, Gd, ctx->stream));
   CKL();
   CK(cudaMemcpyAsync(G, Gd, sizeof(double) * kp1 * kp1, cudaMemcpyDeviceToHost, ctx->stream));

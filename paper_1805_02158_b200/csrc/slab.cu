@@ -8,9 +8,10 @@
 
 namespace redve {
 
-static inline int nblocks(long long n) {
+// enough 256-thread CTAs for 8 per SM (4 for the Gram), fewer for small vectors
+static inline int nblocks(long long n, int cap = SLAB_BLOCKS) {
   long long b = (n + 255) / 256;
-  return (int)(b > 296 ? 296 : (b < 1 ? 1 : b));
+  return (int)(b > cap ? cap : (b < 1 ? 1 : b));
 }
 
 // out[k] (per CTA) for k in [0, K): sums of x*y (DOT), (x-y)^2 (DIST2)
@@ -31,12 +32,12 @@ __global__ void k_vec_reduce(long long n, const double* x, const double* y, doub
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
 }
 
+// one warp: lane-strided sums, then a fixed shuffle tree (deterministic)
 __global__ void k_vec_finish(const double* part, int nb, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < nb; ++i) s += part[i];
-    *out = s;
-  }
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 32) s += part[i];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) *out = s;
 }
 
 void launch_vec_reduce(int op, long long n, const double* x, const double* y, double* part,
@@ -91,77 +92,103 @@ void launch_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, int f,
   k_vec_finish<<<1, 32, 0, s>>>(part, nb, out);
 }
 
-// Gram of the differences of `rows` window vectors (row-major [rows][n]):
-// G[i][j] = sum_p (w_{i+1} - w_i)(w_{j+1} - w_j), i, j < rows-1.  Per-CTA
-// partials, summed in CTA order by k_gram_finish.
-__global__ void k_window_gram(int rows, long long n, const double* w, double* part) {
-  const int kp1 = rows - 1;
-  const int ng = kp1 * (kp1 + 1) / 2;
-  double acc[MAXKP1 * (MAXKP1 + 1) / 2];
-  for (int i = 0; i < ng; ++i) acc[i] = 0.0;
+// Gram of the differences of KP1+1 window vectors (row-major [KP1+1][n]):
+// G[i][j] = sum_p (w_{i+1} - w_i)(w_{j+1} - w_j).  Per-CTA partials (upper
+// triangle, row-major), summed in CTA order by k_gram_finish.
+template <int KP1>
+__global__ void __launch_bounds__(256) k_window_gram(long long n, const double* w, double* part) {
+  constexpr int NG = KP1 * (KP1 + 1) / 2;
+  double acc[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) acc[i] = 0.0;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
        p += (long long)gridDim.x * blockDim.x) {
-    double d[MAXKP1];
-    double prev = w[p];
-    for (int j = 0; j < kp1; ++j) {
-      const double nx = w[(long long)(j + 1) * n + p];
-      d[j] = nx - prev;
-      prev = nx;
-    }
+    double v[KP1 + 1];
+#pragma unroll
+    for (int j = 0; j <= KP1; ++j) v[j] = w[(long long)j * n + p];
+    double d[KP1];
+#pragma unroll
+    for (int j = 0; j < KP1; ++j) d[j] = v[j + 1] - v[j];
     int q = 0;
-    for (int i = 0; i < kp1; ++i)
-      for (int j = i; j < kp1; ++j) {
+#pragma unroll
+    for (int i = 0; i < KP1; ++i)
+#pragma unroll
+      for (int j = i; j < KP1; ++j) {
         acc[q] = fma(d[i], d[j], acc[q]);
         ++q;
       }
   }
   __shared__ double red[32];
-  for (int i = 0; i < ng; ++i) {
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
     double one[1] = {acc[i]};
     block_sum<1>(one, red);
-    if (threadIdx.x == 0) part[(long long)blockIdx.x * ng + i] = one[0];
+    if (threadIdx.x == 0) part[(long long)blockIdx.x * NG + i] = one[0];
   }
 }
+// one warp per Gram entry: lane-strided sums over the CTAs, fixed shuffle tree
 __global__ void k_gram_finish(const double* part, int nb, int kp1, double* G) {
-  if (threadIdx.x || blockIdx.x) return;
   const int ng = kp1 * (kp1 + 1) / 2;
-  int q = 0;
-  for (int i = 0; i < kp1; ++i)
-    for (int j = i; j < kp1; ++j) {
-      double s = 0.0;
-      for (int b = 0; b < nb; ++b) s += part[(long long)b * ng + q];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < ng; q += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += part[(long long)b * ng + q];
+    for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      int i = 0, base = 0;
+      while (q >= base + (kp1 - i)) {
+        base += kp1 - i;
+        ++i;
+      }
+      const int j = i + (q - base);
       G[i * kp1 + j] = s;
       G[j * kp1 + i] = s;
-      ++q;
     }
+  }
 }
 void launch_window_gram(int rows, long long n, const double* w, double* part, double* G,
                         cudaStream_t s) {
-  const int nb = nblocks(n);
-  k_window_gram<<<nb, 256, 0, s>>>(rows, n, w, part);
-  k_gram_finish<<<1, 32, 0, s>>>(part, nb, rows - 1, G);
+  const int nb = nblocks(n, GRAM_BLOCKS);
+  switch (rows - 1) {
+#define GRAM_CASE(K) \
+  case K: k_window_gram<K><<<nb, 256, 0, s>>>(n, w, part); break;
+    GRAM_CASE(1) GRAM_CASE(2) GRAM_CASE(3) GRAM_CASE(4) GRAM_CASE(5) GRAM_CASE(6)
+    GRAM_CASE(7) GRAM_CASE(8) GRAM_CASE(9) GRAM_CASE(10) GRAM_CASE(11) GRAM_CASE(12)
+#undef GRAM_CASE
+    default: return;
+  }
+  k_gram_finish<<<1, 256, 0, s>>>(part, nb, rows - 1, G);
 }
 
-// out = w_0 + sum_{j<ke} xi_j (w_{j+1} - w_j)
-__global__ void k_window_combine(long long n, const double* w, int ke, const double* xi,
-                                 double* out) {
-  __shared__ double s_xi[MAXKP1];
-  if (threadIdx.x < ke) s_xi[threadIdx.x] = xi[threadIdx.x];
-  __syncthreads();
+// out = w_0 + sum_{j<KE} xi_j (w_{j+1} - w_j)
+template <int KE>
+__global__ void __launch_bounds__(256) k_window_combine(long long n, const double* w,
+                                                        const double* xi, double* out) {
+  double c[KE];
+#pragma unroll
+  for (int j = 0; j < KE; ++j) c[j] = xi[j];
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
        p += (long long)gridDim.x * blockDim.x) {
-    double prev = w[p], acc = prev;
-    for (int j = 0; j < ke; ++j) {
-      const double nx = w[(long long)(j + 1) * n + p];
-      acc = fma(s_xi[j], nx - prev, acc);
-      prev = nx;
-    }
+    double v[KE + 1];
+#pragma unroll
+    for (int j = 0; j <= KE; ++j) v[j] = w[(long long)j * n + p];
+    double acc = v[0];
+#pragma unroll
+    for (int j = 0; j < KE; ++j) acc = fma(c[j], v[j + 1] - v[j], acc);
     out[p] = acc;
   }
 }
 void launch_window_combine(long long n, const double* w, int ke, const double* xi, double* out,
                            cudaStream_t s) {
-  k_window_combine<<<nblocks(n), 256, 0, s>>>(n, w, ke, xi, out);
+  const int nb = nblocks(n);
+  switch (ke) {
+#define COMB_CASE(K) \
+  case K: k_window_combine<K><<<nb, 256, 0, s>>>(n, w, xi, out); break;
+    COMB_CASE(1) COMB_CASE(2) COMB_CASE(3) COMB_CASE(4) COMB_CASE(5) COMB_CASE(6)
+    COMB_CASE(7) COMB_CASE(8) COMB_CASE(9) COMB_CASE(10) COMB_CASE(11)
+#undef COMB_CASE
+    default: return;
+  }
 }
 
 }  // namespace redve

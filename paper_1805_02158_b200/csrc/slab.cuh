@@ -5,6 +5,9 @@
 
 namespace redve {
 
+constexpr int SLAB_BLOCKS = 1184;  // CTA cap of the streaming reductions (8 per SM)
+constexpr int GRAM_BLOCKS = 592;   // CTA cap of the window Gram (4 per SM)
+
 void launch_vec_reduce(int op, long long n, const double* x, const double* y, double* part,
                        double* out, cudaStream_t s);  // op 0: dot, 1: squared distance
 void launch_vec_axpby(long long n, double a, const double* x, double b, double* y,

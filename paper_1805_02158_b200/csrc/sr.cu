@@ -159,19 +159,215 @@ __global__ void k_pw_maps(PwArgs a, const double* D, double* maps) {
   }
 }
 
-void launch_pw_maps(const PwArgs& a, cudaStream_t s, int* launches, double* maps) {
+// ---- compile-time specialisations (the generic kernels above serve any radii).
+// Offsets are constants after unrolling, tiles have compile-time edges, and
+// blocks whose halo stays inside the image skip the periodic index wrap.
+__device__ __forceinline__ int wrap_fast(int i, int n) {
+  return ((unsigned)i < (unsigned)n) ? i : wrap(i, n);
+}
+
+template <int SR>
+struct HalfPlane {
+  static constexpr int SIDE = 2 * SR + 1;
+  static constexpr int NPOS = (SIDE * SIDE - 1) / 2;
+  __host__ __device__ static constexpr int di(int k) { return ((SIDE * SIDE + 1) / 2 + k) / SIDE - SR; }
+  __host__ __device__ static constexpr int dj(int k) { return ((SIDE * SIDE + 1) / 2 + k) % SIDE - SR; }
+};
+
+constexpr int PW_ROWS = 4;  // output rows per thread (a column strip), 256 threads = 32 x 8 strips
+
+// Raw weights: every thread owns a 4-row column strip of the 32x32 tile and
+// keeps the (4+2PR) x (2PR+1) patch of x around it in registers; for each
+// offset it forms the squared differences, the separable box sums and the
+// exponential without any block synchronisation.
+template <int PR, int SR>
+__global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
+  constexpr int HALO = PR + SR, X = PW_T + 2 * HALO, P = 2 * PR + 1, R = PW_ROWS + 2 * PR;
+  constexpr int NP = HalfPlane<SR>::NPOS;
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W;
+  double* xs = reinterpret_cast<double*>(s_smem);
+  const int i0 = blockIdx.y * PW_T, j0 = blockIdx.x * PW_T;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    xs[idx] = __ldg(x + (long long)wrap_fast(i0 - HALO + ti, H) * W + wrap_fast(j0 - HALO + tj, W));
+  }
+  __syncthreads();
+  const int oj = threadIdx.x & (PW_T - 1);
+  const int oi0 = (threadIdx.x >> 5) * PW_ROWS;
+  const int gj = j0 + oj;
+  if (gj >= W || i0 + oi0 >= H) return;
+  // tile coordinates of the strip's top-left patch element q = p + (-PR, -PR)
+  const int ti0 = oi0 + HALO - PR, tj0 = oj + HALO - PR;
+  double xc[R][P];
+#pragma unroll
+  for (int u = 0; u < R; ++u)
+#pragma unroll
+    for (int v = 0; v < P; ++v) xc[u][v] = xs[(ti0 + u) * X + tj0 + v];
+  const long long N = (long long)H * W;
+  const double inv_box = 1.0 / (P * P);
+  double* w0 = a.w0 + (long long)b * NP * N + (long long)(i0 + oi0) * W + gj;
+  const int rows = min(PW_ROWS, H - (i0 + oi0));
+#pragma unroll 2
+  for (int k = 0; k < NP; ++k) {
+    const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+    double rs[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      double acc = 0.0;
+#pragma unroll
+      for (int v = 0; v < P; ++v) {
+        const double d = xc[u][v] - xs[(ti0 + u + di) * X + tj0 + v + dj];
+        acc += d * d;
+      }
+      rs[u] = acc;
+    }
+#pragma unroll
+    for (int m = 0; m < PW_ROWS; ++m) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < P; ++t) s += rs[m + t];
+      if (m < rows) w0[(long long)k * N + (long long)m * W] = exp(-fmax(s * inv_box, 0.0) * a.inv_h2);
+    }
+  }
+}
+
+// Balancing sweep / application with compile-time offsets:
+//   S(p) = v(p) + sum_k [ w0_k(p) v(p+o_k) + w0_k(p-o_k) v(p-o_k) ]
+template <int SR>
+__global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din, double* Dout,
+                                                    int first, int apply) {
+  constexpr int X = PW_T + 2 * SR, NP = HalfPlane<SR>::NPOS;
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W;
+  double* vs = reinterpret_cast<double*>(s_smem);
+  const int i0 = blockIdx.y * PW_T, j0 = blockIdx.x * PW_T;
+  const long long N = (long long)H * W;
+  const double* Db = Din + (long long)b * N;
+  const double* x = apply ? a.xin.at(b, a.st) : nullptr;
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    const long long o = (long long)wrap_fast(i0 - SR + ti, H) * W + wrap_fast(j0 - SR + tj, W);
+    const double d = first ? 1.0 : __ldg(Db + o);
+    vs[idx] = apply ? d * __ldg(x + o) : d;
+  }
+  __syncthreads();
+  const bool interior = i0 >= SR && j0 >= SR && i0 + PW_T + SR <= H && j0 + PW_T + SR <= W;
+  const double* w0b = a.w0 + (long long)b * NP * N;
+  const int oj = threadIdx.x & (PW_T - 1);
+  const int gj = j0 + oj;
+  if (gj >= W) return;
+  // the block's 8 warps cover 8 consecutive rows per step m, so the rows above
+  // that the mirrored loads w0_k(p - o_k) touch were fetched a step earlier;
+  // the 4 rows of a thread are accumulated together for memory-level parallelism
+  const int cj = oj + SR;
+  int gi[PW_ROWS], ci[PW_ROWS];
+  long long o[PW_ROWS];
+  double S[PW_ROWS];
+#pragma unroll
+  for (int m = 0; m < PW_ROWS; ++m) {
+    const int oi = (threadIdx.x >> 5) + 8 * m;
+    gi[m] = min(i0 + oi, H - 1);  // rows past the image edge compute a throwaway copy
+    ci[m] = gi[m] - i0 + SR;
+    o[m] = (long long)gi[m] * W + gj;
+    S[m] = vs[ci[m] * X + cj];
+  }
+  if (interior) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+      const double* wk = w0b + (long long)k * N;
+      const int sh = di * W + dj;
+      double wp[PW_ROWS], wm[PW_ROWS];
+#pragma unroll
+      for (int m = 0; m < PW_ROWS; ++m) {
+        wp[m] = __ldg(wk + o[m]);
+        wm[m] = __ldg(wk + o[m] - sh);
+      }
+#pragma unroll
+      for (int m = 0; m < PW_ROWS; ++m) {
+        S[m] = fma(wp[m], vs[(ci[m] + di) * X + cj + dj], S[m]);
+        S[m] = fma(wm[m], vs[(ci[m] - di) * X + cj - dj], S[m]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < NP; ++k) {
+      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+      const double* wk = w0b + (long long)k * N;
+      const int cm = wrap_fast(gj - dj, W);
+#pragma unroll
+      for (int m = 0; m < PW_ROWS; ++m) {
+        const double wp = __ldg(wk + o[m]);
+        const double wm = __ldg(wk + (long long)wrap_fast(gi[m] - di, H) * W + cm);
+        S[m] = fma(wp, vs[(ci[m] + di) * X + cj + dj], S[m]);
+        S[m] = fma(wm, vs[(ci[m] - di) * X + cj - dj], S[m]);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < PW_ROWS; ++m) {
+    if (i0 + (int)(threadIdx.x >> 5) + 8 * m >= H) break;
+    const double d = first ? 1.0 : Db[o[m]];
+    if (apply) a.out[(long long)b * N + o[m]] = d * S[m];
+    else Dout[(long long)b * N + o[m]] = d / sqrt(d * S[m]);
+  }
+}
+
+template <int PR, int SR>
+static void pw_pass_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
   dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
-  k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
-  const size_t sm = sizeof(double) * (PW_T + 2 * a.sr) * (PW_T + 2 * a.sr);
+  constexpr int X = PW_T + 2 * (PR + SR);
+  k_pw_weights_t<PR, SR><<<grid, 256, sizeof(double) * X * X, s>>>(a);
+  ++*launches;
+  const size_t sm = sizeof(double) * (PW_T + 2 * SR) * (PW_T + 2 * SR);
   const double* din = a.D0;
   double* dout = a.D1;
   for (int it = 0; it < a.iters; ++it) {
-    k_pw_sweep<<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    k_pw_sweep_t<SR><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    ++*launches;
     din = dout;
     dout = (dout == a.D1) ? a.D0 : a.D1;
   }
+  if (with_apply) {
+    k_pw_sweep_t<SR><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+    ++*launches;
+  }
+}
+
+// true if a specialisation ran; the final D is in D0 if iters is even, else D1
+static bool pw_specialised(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
+#define PW_CASE(PRV, SRV)                                  \
+  if (a.pr == PRV && a.sr == SRV) {                        \
+    pw_pass_t<PRV, SRV>(a, s, launches, with_apply);       \
+    return true;                                           \
+  }
+  PW_CASE(1, 3) PW_CASE(1, 1) PW_CASE(1, 2) PW_CASE(0, 3) PW_CASE(2, 3) PW_CASE(0, 1)
+#undef PW_CASE
+  return false;
+}
+
+void launch_pw_maps(const PwArgs& a, cudaStream_t s, int* launches, double* maps) {
+  dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
+  const double* din = a.D0;
+  if (pw_specialised(a, s, launches, false)) {
+    din = (a.iters % 2 == 0) ? a.D0 : a.D1;
+  } else {
+    k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
+    const size_t sm = sizeof(double) * (PW_T + 2 * a.sr) * (PW_T + 2 * a.sr);
+    double* dout = a.D1;
+    for (int it = 0; it < a.iters; ++it) {
+      k_pw_sweep<<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+      din = dout;
+      dout = (dout == a.D1) ? a.D0 : a.D1;
+    }
+    *launches += a.iters + 1;
+  }
   k_pw_maps<<<dim3(cdivs((long long)a.H * a.W, 256), a.B), 256, 0, s>>>(a, din, maps);
-  *launches += a.iters + 2;
+  ++*launches;
 }
 
 size_t pw_weights_smem(int pr, int sr) {
@@ -180,6 +376,7 @@ size_t pw_weights_smem(int pr, int sr) {
 }
 
 void launch_pw(const PwArgs& a, cudaStream_t s, int* launches) {
+  if (pw_specialised(a, s, launches, true)) return;
   dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
   k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
   ++*launches;
@@ -198,9 +395,12 @@ void launch_pw(const PwArgs& a, cudaStream_t s, int* launches) {
 
 // --------------------------------------------------------------- normal operator
 // (A w)(u,v) = (1/sigma^2) (H^T H w)(u,v) + alpha w(u,v),  H = keep(== 0 mod s) o conv.
-// Tile: TH x TW outputs, w tile with halo 2r, zero-filled LR samples z_up with
-// halo r, both in shared memory.
-constexpr int MV_TH = 16, MV_TW = 32;
+// Tile: TH x TW outputs, w tile with halo 2r in shared memory.  Only the
+// measurement-lattice samples of z = H w inside the tile's reach are formed
+// (a compact lattice list, periodic seams included), and each output gathers
+// the <= ceil((2r+1)/s)^2 lattice samples in its window -- the same terms, in
+// the same order, as the dense correlation with the zero-filled z_up.
+constexpr int MV_TH = 32, MV_TW = 32;
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
@@ -215,11 +415,16 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
   }
   const int H = a.H, W = a.W, s = a.factor, k = a.k, r = k / 2;
   const int WX = MV_TW + 4 * r, HX = MV_TH + 4 * r;  // w tile
-  const int WZ = MV_TW + 2 * r, HZ = MV_TH + 2 * r;  // z_up tile
+  const int WZ = MV_TW + 2 * r, HZ = MV_TH + 2 * r;  // z_up window
   double* taps = reinterpret_cast<double*>(s_smem);
   double* ws = taps + k * k;
-  double* zs = ws + HX * WX;
-  double* red = zs + HZ * WZ;
+  double* zc = ws + HX * WX;                // compact lattice samples [nzr][nzc]
+  double* red = zc + HZ * WZ;
+  int* zr_pos = reinterpret_cast<int*>(red + 64);  // lattice rows / cols (window coords)
+  int* zc_pos = zr_pos + HZ;
+  int* rwin = zc_pos + WZ;                  // per output row: first lattice row, count
+  int* cwin = rwin + 2 * MV_TH;             // (rwin doubles as flag scratch: >= 64 + WZ ints)
+  __shared__ int s_nzr, s_nzc;
   for (int i = threadIdx.x; i < k * k; i += blockDim.x) taps[i] = a.taps[i];
   const long long N = (long long)H * W;
   const int i0 = blockIdx.y * MV_TH, j0 = blockIdx.x * MV_TW;
@@ -229,27 +434,65 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
   const double* xin = (MODE == CG_ITER) ? nullptr : a.xin.at(b, a.st);
   for (int idx = threadIdx.x; idx < HX * WX; idx += blockDim.x) {
     const int ti = idx / WX, tj = idx - ti * WX;
-    const long long o = (long long)wrap(i0 - 2 * r + ti, H) * W + wrap(j0 - 2 * r + tj, W);
+    const long long o =
+        (long long)wrap_fast(i0 - 2 * r + ti, H) * W + wrap_fast(j0 - 2 * r + tj, W);
     double w;
     if (MODE == CG_ITER) w = (a.it > 0) ? fma(beta, pold[o], rr[o]) : rr[o];
     else w = xin[o];
     ws[idx] = w;
   }
-  __syncthreads();
-  // z_up(u, v) = (H w)(u, v) at measurement-grid points, 0 elsewhere
-  for (int idx = threadIdx.x; idx < HZ * WZ; idx += blockDim.x) {
-    const int zi = idx / WZ, zj = idx - zi * WZ;
-    const int gu = wrap(i0 - r + zi, H), gv = wrap(j0 - r + zj, W);
-    // measurement lattice by GLOBAL row (a slab of a spatially split image
-    // starts at global row a.row0 of an a.Hg-row image)
+  // lattice rows / columns of the window: measurement lattice by GLOBAL row
+  // (a slab of a spatially split image starts at global row a.row0 of an
+  // a.Hg-row image)
+  int* flag = rwin;  // scratch: lattice flags of window rows [0, HZ) and columns [64, 64 + WZ)
+  if (threadIdx.x < HZ) {
+    const int gu = wrap_fast(i0 - r + (int)threadIdx.x, H);
     const int gg = (a.Hg > 0) ? (int)(((long long)a.row0 + gu) % a.Hg) : gu;
+    flag[threadIdx.x] = (gg % s) == 0;
+  } else if (threadIdx.x >= 64 && threadIdx.x < 64 + WZ) {
+    flag[threadIdx.x] = (wrap_fast(j0 - r + (int)threadIdx.x - 64, W) % s) == 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int zi = 0; zi < HZ; ++zi)
+      if (flag[zi]) zr_pos[n++] = zi;
+    s_nzr = n;
+  } else if (threadIdx.x == 32) {
+    int n = 0;
+    for (int zj = 0; zj < WZ; ++zj)
+      if (flag[64 + zj]) zc_pos[n++] = zj;
+    s_nzc = n;
+  }
+  __syncthreads();
+  const int nzr = s_nzr, nzc = s_nzc;
+  // output row u (tile coords) reads window rows [u, u + 2r]
+  if (threadIdx.x < MV_TH) {
+    const int u = threadIdx.x;
+    int first = 0;
+    while (first < nzr && zr_pos[first] < u) ++first;
+    int last = first;
+    while (last < nzr && zr_pos[last] <= u + 2 * r) ++last;
+    rwin[2 * u] = first;
+    rwin[2 * u + 1] = last - first;
+  } else if (threadIdx.x >= 64 && threadIdx.x < 64 + MV_TW) {
+    const int v = threadIdx.x - 64;
+    int first = 0;
+    while (first < nzc && zc_pos[first] < v) ++first;
+    int last = first;
+    while (last < nzc && zc_pos[last] <= v + 2 * r) ++last;
+    cwin[2 * v] = first;
+    cwin[2 * v + 1] = last - first;
+  }
+  // z = H w at the lattice samples
+  for (int idx = threadIdx.x; idx < nzr * nzc; idx += blockDim.x) {
+    const int li = idx / nzc, lj = idx - li * nzc;
+    const int zi = zr_pos[li], zj = zc_pos[lj];
     double z = 0.0;
-    if ((gg % s) == 0 && (gv % s) == 0) {
-      for (int ta = 0; ta < k; ++ta)
-        for (int tb = 0; tb < k; ++tb)
-          z = fma(taps[ta * k + tb], ws[(zi + r - (ta - r)) * WX + (zj + r - (tb - r))], z);
-    }
-    zs[idx] = z;
+    for (int ta = 0; ta < k; ++ta)
+      for (int tb = 0; tb < k; ++tb)
+        z = fma(taps[ta * k + tb], ws[(zi + r - (ta - r)) * WX + (zj + r - (tb - r))], z);
+    zc[idx] = z;
   }
   __syncthreads();
   double acc[2] = {0.0, 0.0};
@@ -258,10 +501,14 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
     const int oi = idx / MV_TW, oj = idx - oi * MV_TW;
     const int gi = i0 + oi, gj = j0 + oj;
     if (gi >= H || gj >= W) continue;
-    double ht = 0.0;  // (H^T z_up)(u, v): correlation
-    for (int ta = 0; ta < k; ++ta)
-      for (int tb = 0; tb < k; ++tb)
-        ht = fma(taps[ta * k + tb], zs[(oi + r + (ta - r)) * WZ + (oj + r + (tb - r))], ht);
+    double ht = 0.0;  // (H^T z_up)(u, v): correlation over the window's lattice samples
+    const int rf = rwin[2 * oi], rn = rwin[2 * oi + 1];
+    const int cf = cwin[2 * oj], cn = cwin[2 * oj + 1];
+    for (int i = rf; i < rf + rn; ++i) {
+      const double* trow = taps + (zr_pos[i] - oi) * k - oj;
+      const double* zrow = zc + i * nzc;
+      for (int j = cf; j < cf + cn; ++j) ht = fma(trow[zc_pos[j]], zrow[j], ht);
+    }
     const double wv = ws[(oi + 2 * r) * WX + (oj + 2 * r)];
     const double aw = fma(ht, inv_s2, a.alpha * wv);
     const long long o = (long long)b * N + (long long)gi * W + gj;
@@ -374,7 +621,8 @@ __global__ void k_cg_zero_b(CgArgs a) {
 size_t cg_matvec_smem(int k) {
   const int r = k / 2;
   return sizeof(double) * ((size_t)k * k + (size_t)(MV_TH + 4 * r) * (MV_TW + 4 * r) +
-                           (size_t)(MV_TH + 2 * r) * (MV_TW + 2 * r) + 64);
+                           (size_t)(MV_TH + 2 * r) * (MV_TW + 2 * r) + 64) +
+         sizeof(int) * ((size_t)(MV_TH + 2 * r) + (MV_TW + 2 * r) + 2 * MV_TH + 2 * MV_TW + 64);
 }
 
 template <int MODE>
@@ -392,7 +640,7 @@ static void matvec_t(const CgArgs& a, cudaStream_t s) {
 int cg_matvec_blocks(int H, int W) { return cdivs(W, MV_TW) * cdivs(H, MV_TH); }
 int cg_update_blocks(long long N) {
   int c = cdivs(N, 256 * 8);
-  return c > 256 ? 256 : (c < 1 ? 1 : c);
+  return c > 1184 ? 1184 : (c < 1 ? 1 : c);
 }
 
 void launch_cg_init(const CgArgs& a, cudaStream_t s) { matvec_t<CG_INIT>(a, s); }

@@ -269,14 +269,23 @@ class SpatialProblem:
         self.ref = None if reference is None else self.ops.tensor(
             np.asarray(reference, dtype=np.float64)[lay.start: lay.stop])
         self.N = H * W
+        self._ext = {}
 
     # -- helpers
     def slab(self, x_global):
+        """This rank's rows of a host image (a device tensor is taken as the slab itself)."""
+        if hasattr(x_global, "is_cuda") or hasattr(x_global, "clone"):
+            if tuple(x_global.shape) != (self.lay.rows, self.W):
+                raise ValueError(f"slab tensor must be {(self.lay.rows, self.W)}")
+            return x_global.clone()
         return self.ops.tensor(np.asarray(x_global, dtype=np.float64)[self.lay.start: self.lay.stop])
 
-    def extend(self, x):
+    def extend(self, x, slot="x"):
+        """x with its halos from the ring, in a persistent per-slot buffer."""
         lay = self.lay
-        ext = self.ops.zeros((lay.Hext, self.W))
+        ext = self._ext.get(slot)
+        if ext is None:
+            ext = self._ext[slot] = self.ops.zeros((lay.Hext, self.W))
         ext[lay.halo: lay.halo + lay.rows].copy_(x)
         self.comm.exchange(ext, lay.halo, lay.rows)
         return ext
@@ -289,7 +298,7 @@ class SpatialProblem:
         return self.comm.allreduce([self.ops.dot(a, b) for a, b in pairs])
 
     def matvec(self, p):
-        ext = self.extend(p)
+        ext = self.extend(p, "p")
         return self.interior(self.ops.normal_matvec(ext, self.lay.row0, self.H)).contiguous()
 
     # -- objective pieces (objective.py:78-121 on slabs)

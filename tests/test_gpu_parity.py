@@ -270,7 +270,7 @@ class TestSuperres:
                 n += 1
         assert n >= 3
 
-    @pytest.mark.parametrize("shape", [(32, 40), (96, 96), (70, 33)])
+    @pytest.mark.parametrize("shape", [(32, 40), (96, 96), (70, 33), (200, 170), (5, 7)])
     def test_patch_weighted_vs_oracle(self, rv, R, shape):
         x = np.random.default_rng(7).uniform(0, 255, shape)
         assert rel(rv.PatchWeighted()(x), R.patch_weighted(x)) <= 1e-12
