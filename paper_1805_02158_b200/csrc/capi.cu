@@ -947,6 +947,26 @@ int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* c
   return REDVE_OK;
 }
 
+// CTAs per image for the VE passes (k_gram / k_combine, 256 threads, 2 resident
+// per SM): minimise waves x (pixels per thread + the per-CTA reduction cost),
+// so small batches still fill the GPU and large ones are not cut into slivers.
+static int ve_chunks(int B, long long N) {
+  const long long resident = 2LL * 148;
+  int best = 1;
+  double best_cost = 1e300;
+  for (int c = 1; c <= 64; ++c) {
+    if ((long long)c * 256 > N && c > 1) break;
+    const long long ctas = (long long)B * c;
+    const double waves = (double)((ctas + resident - 1) / resident);
+    const double cost = waves * ((double)N / (256.0 * c) + 6.0);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = c;
+    }
+  }
+  return best;
+}
+
 // ------------------------------------------------------------------ solve
 int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x0, double* x_out,
                 redve_trace* trace) {
@@ -983,9 +1003,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
 
   CK(p->ring.ensure(sizeof(double) * N * S * B));
   if (track) CK(p->best.ensure(sizeof(double) * N * B));
-  int chunks = (int)((N + 256 * 8 - 1) / (256 * 8));
-  if (chunks > 64) chunks = 64;
-  if (chunks < 1) chunks = 1;
+  const int chunks = ve_chunks(B, N);
   if (ve) {
     CK(p->q.ensure(sizeof(double) * N * kp1 * B));
     size_t need = (size_t)B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2);
@@ -1258,9 +1276,7 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
   CKL();
   RUN(ctx, "window_extrapolate_setup", launch_window_extrapolate_setup(st, B, rows, 0, s));
   CKL();
-  int chunks = (int)((n + 256 * 8 - 1) / (256 * 8));
-  if (chunks > 64) chunks = 64;
-  if (chunks < 1) chunks = 1;
+  const int chunks = ve_chunks(B, n);
   CK(ctx->ve_partials.ensure(sizeof(double) * B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2) + 64));
   CK(ctx->ve_counters.ensure(sizeof(unsigned) * B));
   CK(cudaMemsetAsync(ctx->ve_counters.p, 0, sizeof(unsigned) * B, s));

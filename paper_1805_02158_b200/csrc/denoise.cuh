@@ -49,6 +49,10 @@ __device__ __forceinline__ int wrap(int i, int n) {
   i %= n;
   return i < 0 ? i + n : i;
 }
+// periodic index, cheap when already in range (tile halos mostly are)
+__device__ __forceinline__ int wrap_fast(int i, int n) {
+  return ((unsigned)i < (unsigned)n) ? i : wrap(i, n);
+}
 
 // f at (tile row ti, column c) for both images of the pair.  `tile` is
 // [rows][W] complex; `taps` in shared memory.

@@ -64,6 +64,98 @@ __global__ void __launch_bounds__(256) k_rd_denoise(RdArgs a) {
   }
 }
 
+// Register-blocked specialisation for FS x FS filters: per filter, the
+// influence response on the tile + halo r is formed by column strips of
+// RD_S1 rows (each loaded x column segment feeds FS*RD_S1 FMAs), written to
+// a double-buffered shared tile, and the adjoint filter is accumulated into
+// RD_S2-row output strips held in registers across all filters.
+constexpr int RD_S1 = 6, RD_S2 = 4;
+
+template <int FS>
+__global__ void __launch_bounds__(256) k_rd_fast(RdArgs a) {
+  constexpr int R = FS / 2, X = RD_T + 4 * R, P = RD_T + 2 * R;
+  constexpr int NS1 = (P + RD_S1 - 1) / RD_S1;
+  static_assert(RD_T * RD_T == 256 * RD_S2, "one output strip per thread");
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W, nf = a.nf;
+  double* ks = reinterpret_cast<double*>(r_smem);
+  double* sc = ks + nf * FS * FS;
+  double* xs = sc + nf;
+  double* ph = xs + X * X;  // [2][P][P]
+  for (int i = threadIdx.x; i < nf * FS * FS; i += blockDim.x) ks[i] = a.filters[i];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) sc[i] = 1.0 / (a.scales[i] * a.scales[i]);
+  const int i0 = blockIdx.y * RD_T, j0 = blockIdx.x * RD_T;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    xs[idx] = __ldg(x + (long long)wrap_fast(i0 - 2 * R + ti, H) * W + wrap_fast(j0 - 2 * R + tj, W));
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const bool p1 = t < NS1 * P;
+  const int pc = t % P, pr0 = (t / P) * RD_S1;
+  const int oc = t & (RD_T - 1), or0 = (t >> 5) * RD_S2;
+  double acc[RD_S2];
+#pragma unroll
+  for (int m = 0; m < RD_S2; ++m) acc[m] = 0.0;
+  for (int f = 0; f < nf; ++f) {
+    double* phb = ph + (f & 1) * P * P;
+    const double* kf = ks + f * FS * FS;
+    if (p1) {  // phi_f(q) = z / (1 + z^2/s^2), z = sum_ab k[a][b] x(q + (a-r, b-r))
+      double z[RD_S1];
+#pragma unroll
+      for (int m = 0; m < RD_S1; ++m) z[m] = 0.0;
+#pragma unroll
+      for (int tb = 0; tb < FS; ++tb) {
+        double v[RD_S1 + FS - 1];
+#pragma unroll
+        for (int u = 0; u < RD_S1 + FS - 1; ++u)
+          v[u] = (P % RD_S1 == 0 || pr0 + u < X) ? xs[(pr0 + u) * X + pc + tb] : 0.0;
+#pragma unroll
+        for (int ta = 0; ta < FS; ++ta) {
+          const double kk = kf[ta * FS + tb];
+#pragma unroll
+          for (int m = 0; m < RD_S1; ++m) z[m] = fma(kk, v[m + ta], z[m]);
+        }
+      }
+      const double sf = sc[f];
+#pragma unroll
+      for (int m = 0; m < RD_S1; ++m)
+        if (P % RD_S1 == 0 || pr0 + m < P) phb[(pr0 + m) * P + pc] = z[m] / fma(z[m] * z[m], sf, 1.0);
+    }
+    __syncthreads();
+    // adjoint: acc(p) += sum_ab k[a][b] phi(p - (a-r, b-r))
+#pragma unroll
+    for (int tb = 0; tb < FS; ++tb) {
+      double v[RD_S2 + FS - 1];
+#pragma unroll
+      for (int u = 0; u < RD_S2 + FS - 1; ++u) v[u] = phb[(or0 + u) * P + oc + 2 * R - tb];
+#pragma unroll
+      for (int ta = 0; ta < FS; ++ta) {
+        const double kk = kf[ta * FS + tb];
+#pragma unroll
+        for (int m = 0; m < RD_S2; ++m) acc[m] = fma(kk, v[m + 2 * R - ta], acc[m]);
+      }
+    }
+  }
+  const long long N = (long long)H * W;
+  const int gj = j0 + oc;
+#pragma unroll
+  for (int m = 0; m < RD_S2; ++m) {
+    const int gi = i0 + or0 + m;
+    if (gi >= H || gj >= W) continue;
+    const double xv = xs[(or0 + m + 2 * R) * X + (oc + 2 * R)];
+    a.out[(long long)b * N + (long long)gi * W + gj] = fma(-a.tau, acc[m], xv);
+  }
+}
+
+template <int FS>
+static size_t rd_fast_smem(int nf) {
+  constexpr int R = FS / 2, X = RD_T + 4 * R, P = RD_T + 2 * R;
+  return sizeof(double) * ((size_t)nf * FS * FS + nf + (size_t)X * X + 2 * (size_t)P * P);
+}
+
 size_t rd_smem(int nf, int fs) {
   const int r = fs / 2, X = RD_T + 4 * r, P = RD_T + 2 * r;
   return sizeof(double) * ((size_t)nf * fs * fs + nf + (size_t)X * X + (size_t)nf * P * P);
@@ -73,10 +165,18 @@ void launch_rd(const RdArgs& a, cudaStream_t s) {
   static bool done = false;
   if (!done) {
     cudaFuncSetAttribute(k_rd_denoise, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_rd_fast<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_rd_fast<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_rd_fast<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
   }
   dim3 grid((a.W + RD_T - 1) / RD_T, (a.H + RD_T - 1) / RD_T, a.B);
-  k_rd_denoise<<<grid, 256, rd_smem(a.nf, a.fs), s>>>(a);
+  switch (a.fs) {
+    case 3: k_rd_fast<3><<<grid, 256, rd_fast_smem<3>(a.nf), s>>>(a); return;
+    case 5: k_rd_fast<5><<<grid, 256, rd_fast_smem<5>(a.nf), s>>>(a); return;
+    case 7: k_rd_fast<7><<<grid, 256, rd_fast_smem<7>(a.nf), s>>>(a); return;
+    default: k_rd_denoise<<<grid, 256, rd_smem(a.nf, a.fs), s>>>(a);
+  }
 }
 
 }  // namespace redve

@@ -162,9 +162,6 @@ __global__ void k_pw_maps(PwArgs a, const double* D, double* maps) {
 // ---- compile-time specialisations (the generic kernels above serve any radii).
 // Offsets are constants after unrolling, tiles have compile-time edges, and
 // blocks whose halo stays inside the image skip the periodic index wrap.
-__device__ __forceinline__ int wrap_fast(int i, int n) {
-  return ((unsigned)i < (unsigned)n) ? i : wrap(i, n);
-}
 
 template <int SR>
 struct HalfPlane {
