@@ -237,6 +237,9 @@ struct redve_problem {
   DevBuf rd_filters, rd_scales;
   DevBuf htaps, dntaps, y, ref, hty, xb, g, Z, state, partials, cnt_inv, cnt_cost, cnt_ve,
       fbuf, ring, best, q, trace, vals;
+  // Fourier-route cost identity: f(x_{k-1}) of cadence steps, second f buffer
+  // for the precomputed denoisers, ||y||^2 per image
+  DevBuf fprev, fcur, yy;
   bool has_ref = false;
   const cd* twH = nullptr;
   const cd* twW = nullptr;
@@ -279,10 +282,11 @@ static int map_dn_kind(int k) {
 
 // Fourier solve pipeline on pairs: Z <- rowfwd(xin) ; col(scale) ; rowinv -> out
 // The three Fourier kernels as separate pieces.
-static int f_row_fwd(redve_problem* p, View xin, DenoiseArgs dn, cd* Z, int phase) {
+static int f_row_fwd(redve_problem* p, View xin, DenoiseArgs dn, cd* Z, int phase,
+                     double* fout = nullptr) {
   redve_ctx* ctx = p->ctx;
   RowFwdArgs rf{p->B, p->H, p->W, p->lpc_row, xin, dn, Z, p->twW, p->twsW,
-                p->state.as<ImgState>(), phase};
+                p->state.as<ImgState>(), phase, fout};
   RUN(ctx, "row_fwd", launch_row_fwd(rf, p->npairs, ctx->stream));
   CKL();
   return REDVE_OK;
@@ -328,13 +332,14 @@ static View plain(const double* base, long long N) {
 
 // f(x) into p->fbuf for the device denoisers the Fourier kernels do not fuse
 // (PatchWeighted always; the stencils on the CG route).
-static int denoise_to_fbuf(redve_problem* p, View x, int phase) {
+static int denoise_to_fbuf(redve_problem* p, View x, int phase, double* out = nullptr) {
   redve_ctx* ctx = p->ctx;
+  double* fdst = out ? out : p->fbuf.as<double>();
   if (p->dn_api_kind == REDVE_DN_FILTERBANK) {
     RdArgs a;
     a.B = p->B; a.H = p->H; a.W = p->W; a.nf = p->rd_nf; a.fs = p->rd_fs;
     a.filters = p->rd_filters.as<double>(); a.scales = p->rd_scales.as<double>(); a.tau = p->rd_tau;
-    a.xin = x; a.out = p->fbuf.as<double>(); a.st = p->state.as<ImgState>(); a.phase = phase;
+    a.xin = x; a.out = fdst; a.st = p->state.as<ImgState>(); a.phase = phase;
     RUN(ctx, "filter_bank", launch_rd(a, ctx->stream));
   } else if (p->dn_api_kind == REDVE_DN_PATCH) {
     PwArgs a;
@@ -343,13 +348,13 @@ static int denoise_to_fbuf(redve_problem* p, View x, int phase) {
     a.inv_h2 = 1.0 / (p->pw_h * p->pw_h);
     a.xin = x;
     a.w0 = p->w0.as<double>(); a.D0 = p->D0.as<double>(); a.D1 = p->D1.as<double>();
-    a.out = p->fbuf.as<double>();
+    a.out = fdst;
     a.st = p->state.as<ImgState>(); a.phase = phase;
     int n = 0;
     RUN(ctx, "patch_weighted", launch_pw(a, ctx->stream, &n));
     g_launches.fetch_add(n - 1);
   } else {
-    RUN(ctx, "denoise", launch_denoise_view(x, dn_args(p), p->fbuf.as<double>(),
+    RUN(ctx, "denoise", launch_denoise_view(x, dn_args(p), fdst,
                                             p->state.as<ImgState>(), phase, p->B, p->H, p->W,
                                             ctx->stream));
   }
@@ -774,7 +779,11 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), B, s));
   int nblk_row = (H + p->lpc_row - 1) / p->lpc_row;
   int nblk_cost = (H + cost_rows(H) - 1) / cost_rows(H);
-  size_t part = (size_t)p->npairs * (nblk_row > nblk_cost ? nblk_row : nblk_cost) * 6;
+  int nblk_fp = (H + cost_fp_rows(W) - 1) / cost_fp_rows(W);
+  int nblk_max = nblk_row > nblk_cost ? nblk_row : nblk_cost;
+  if (nblk_fp > nblk_max) nblk_max = nblk_fp;
+  size_t part = (size_t)p->npairs * nblk_max * 8;
+  if (part < (size_t)B * 64 * 4) part = (size_t)B * 64 * 4;  // k_cost_fp: <= 64 CTAs per image
   PK(p->partials.ensure(sizeof(double) * part));
   PK(p->cnt_inv.ensure(sizeof(unsigned) * (B + 1)));
   PK(p->cnt_cost.ensure(sizeof(unsigned) * (B + 1)));
@@ -848,6 +857,13 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
                              plain(p->xb.as<double>(), p->N), nullptr, 0, plain(nullptr, p->N),
                              ctl, tr, 1, PH_SETUP);
     if (r) return bail(r);
+    // cost identity on the Fourier route (cost.cu k_cost_fp)
+    PK(p->fprev.ensure(sizeof(double) * p->N * B));
+    PK(p->yy.ensure(sizeof(double) * B));
+    RUN(ctx, "sumsq", launch_sumsq(p->y.as<double>(), Ny, B, p->yy.as<double>(), s));
+    PK(cudaGetLastError());
+    if (dn->kind == REDVE_DN_PATCH || dn->kind == REDVE_DN_FILTERBANK)
+      PK(p->fcur.ensure(sizeof(double) * p->N * B));
   }
 #undef PK
   *out = p;
@@ -1068,17 +1084,40 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
     va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
 
-    // cost evaluation of the current iterates: PatchWeighted needs f(x) first
+    // Cost of the current iterates.  Fourier route: cadence records use the
+    // normal-equation identity (k_cost_fp) with f(x_{k-1}) kept by k_row_fwd
+    // (fused denoisers) or by the step itself (precomputed denoisers).  For the
+    // precomputed denoisers f(x_k) evaluated here is handed to the next step
+    // when nothing changes the iterate in between (f_ready).
+    const bool ident = p->fourier;
+    double* f_step = p->fbuf.as<double>();   // f of the current step's input
+    double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
+    bool f_ready = false;
     auto cost_of_cur = [&](int mode, StepCtl c) -> int {
       const double* fe = nullptr;
+      const int ph = mode == COST_RECORD ? c.phase : PH_SETUP;
       if (pw) {
-        int r = denoise_to_fbuf(p, cur, mode == COST_RECORD ? c.phase : PH_SETUP);
+        double* dst = ident ? f_spare : p->fbuf.as<double>();
+        int r = denoise_to_fbuf(p, cur, ph, dst);
         if (r) return r;
-        fe = p->fbuf.as<double>();
+        fe = dst;
       }
       CostArgs ca = cost_args(p, cur, fe, mode, c, tr);
-      RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
+      if (ident && mode == COST_RECORD) {
+        ca.fprev = pw ? f_step : p->fprev.as<double>();
+        ca.hty = p->hty.as<double>();
+        ca.yy = p->yy.as<double>();
+      }
+      if (ident && mode == COST_RECORD && cost_fp_ok(ca)) {
+        RUN(ctx, "cost", launch_cost_fp(ca, p->npairs, s));
+      } else {
+        RUN(ctx, "cost", launch_cost(ca, p->npairs, s));
+      }
       CKL();
+      if (pw && ident && mode != COST_FINAL) {  // f(cur) is ready for the next step
+        std::swap(f_step, f_spare);
+        f_ready = true;
+      }
       return REDVE_OK;
     };
 
@@ -1100,13 +1139,17 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
           View xin = cur;
           DenoiseArgs d = dn;
           if (pw) {
-            r = denoise_to_fbuf(p, cur, phase);
-            if (r) return r;
-            xin = plain(p->fbuf.as<double>(), N);
+            if (!f_ready) {
+              r = denoise_to_fbuf(p, cur, phase, f_step);
+              if (r) return r;
+            }
+            xin = plain(f_step, N);
             d.kind = DN_IDENTITY;
             d.radius = 0;
           }
-          if ((r = f_row_fwd(p, xin, d, zc, phase))) return r;
+          f_ready = false;
+          double* fout = (cadence && !pw) ? p->fprev.as<double>() : nullptr;
+          if ((r = f_row_fwd(p, xin, d, zc, phase, fout))) return r;
         }
         if ((r = f_col(p, zc, p->alpha, phase))) return r;
         r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
@@ -1171,6 +1214,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
           CKL();
           RUN(ctx, "combine", launch_combine(va, s));
           CKL();
+          f_ready = false;  // the iterate may have been replaced
         }
         if (k >= budget) break;
         if (++cycles % check_every == 0 && !use_graph) {

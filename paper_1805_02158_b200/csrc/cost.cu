@@ -226,4 +226,176 @@ void launch_cost_fast(const CostArgs& a, int npairs, cudaStream_t s) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fourier-route objective by the normal-equation identity.  x = x_k is the
+// exact solution of (H^T H / s^2 + a I) x = H^T y / s^2 + a f, f = f(x_{k-1})
+// (objective.py:100-104), so H^T H x = H^T y + a s^2 (f - x) and
+//   ||Hx - y||^2 = ||y||^2 - s^2 <x, H^T y / s^2> + a s^2 <x, f - x>
+// -- no blur of x.  A streaming pass: each thread owns a pair of adjacent
+// pixels of one image, forms f(x_k) from L1-resident neighbours (median /
+// stencil) or reads it (precomputed denoisers), and reads f(x_{k-1}) (kept by
+// k_row_fwd), H^T y / s^2 and the reference with coalesced 16-byte loads.
+int cost_fp_rows(int W) {  // kept for the partials sizing of the problem
+  int rows = 2048 / W;
+  return rows < 1 ? 1 : rows;
+}
+
+bool cost_fp_ok(const CostArgs& a) {
+  return a.fprev && a.hty && a.yy && (a.W % 2) == 0 && a.W >= 4 && a.H >= 3 && a.factor == 1 &&
+         (a.dn.kind != DN_CONV || a.dn.ksize <= 7);
+}
+
+static int cost_fp_chunks(int B, long long N) {
+  int c = (int)((1184 + B - 1) / B);
+  const long long per = (N / 2 + 255) / 256;  // CTA-passes per image
+  if (c > per) c = (int)per;
+  if (c > 64) c = 64;
+  return c < 1 ? 1 : c;
+}
+
+template <int DK>
+__device__ __forceinline__ void fk_pair(const double* x, int H, int W, int i, int j,
+                                        const DenoiseArgs& dn, const double* taps,
+                                        double& f0, double& f1) {
+  if (DK == DN_MEDIAN3) {
+    const int im = wrap_fast(i - 1, H), ip = wrap_fast(i + 1, H);
+    const int jm = edge_wrap(j - 1, W), jp = edge_wrap(j + 2, W);
+    const double* r0 = x + (long long)im * W;
+    const double* r1 = x + (long long)i * W;
+    const double* r2 = x + (long long)ip * W;
+    double c[4][3];
+    const int cols[4] = {jm, j, j + 1, jp};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double a = __ldg(r0 + cols[q]), b = __ldg(r1 + cols[q]), e = __ldg(r2 + cols[q]);
+      sort2(a, b);
+      sort2(b, e);
+      sort2(a, b);
+      c[q][0] = a;
+      c[q][1] = b;
+      c[q][2] = e;
+    }
+    f0 = med3d(dmax(dmax(c[0][0], c[1][0]), c[2][0]), med3d(c[0][1], c[1][1], c[2][1]),
+               dmin(dmin(c[0][2], c[1][2]), c[2][2]));
+    f1 = med3d(dmax(dmax(c[1][0], c[2][0]), c[3][0]), med3d(c[1][1], c[2][1], c[3][1]),
+               dmin(dmin(c[1][2], c[2][2]), c[3][2]));
+  } else if (DK == DN_CONV) {
+    const int k = dn.ksize, r = k >> 1;
+    double a0 = 0.0, a1 = 0.0;
+    for (int ta = 0; ta < k; ++ta) {
+      const double* row = x + (long long)wrap_fast(i - (ta - r), H) * W;
+      for (int tb = 0; tb < k; ++tb) {
+        const double w = taps[ta * k + tb];
+        a0 = fma(w, __ldg(row + wrap_fast(j - (tb - r), W)), a0);
+        a1 = fma(w, __ldg(row + wrap_fast(j + 1 - (tb - r), W)), a1);
+      }
+    }
+    f0 = a0;
+    f1 = a1;
+  } else {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(x + (long long)i * W + j));
+    f0 = v.x;
+    f1 = v.y;
+  }
+}
+
+template <int DK>
+__global__ void __launch_bounds__(256) k_cost_fp(CostArgs a) {
+  const int b = blockIdx.y;
+  ImgState& st = a.st[b];
+  const bool want = cost_wants(st, a);
+  const int nblk = gridDim.x;
+  if (!want) {
+    if (a.mode == COST_RECORD && blockIdx.x == 0 && threadIdx.x == 0) commit_step(st, a.ctl.phase);
+    return;
+  }
+  __shared__ double s_taps[64];
+  __shared__ double s_red[32 * 4];
+  const int kk = DK == DN_CONV ? a.dn.ksize * a.dn.ksize : 0;
+  for (int i = threadIdx.x; i < kk && i < 64; i += blockDim.x) s_taps[i] = a.dn.taps[i];
+  if (DK == DN_CONV) __syncthreads();
+  const int H = a.H, W = a.W;
+  const long long N = (long long)H * W;
+  const double* x = a.x.at(b, a.st);
+  const double* fx = DK == DN_EXTERNAL ? a.fext + (long long)b * N : x;
+  const double* hp = a.hty + (long long)b * N;
+  const double* fp = a.fprev + (long long)b * N;
+  const double* rp = a.ref ? a.ref + (long long)b * N : nullptr;
+  const int W2 = W >> 1;
+  const long long P = N >> 1;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // reg, <x,hty>, <x,fprev-x>, ssd
+  // grid-stride over pixel pairs with the (row, pair) position advanced
+  // incrementally (no division in the loop)
+  const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)nblk * blockDim.x;
+  const int di = (int)(stride / W2), dj = (int)(stride % W2);
+  int i = (int)(q0 / W2), j2 = (int)(q0 % W2);
+  for (long long q = q0; q < P; q += stride) {
+    const int j = 2 * j2;
+    const long long o = (long long)i * W + j;
+    const double2 xv = __ldg(reinterpret_cast<const double2*>(x + o));
+    const double2 hv = __ldg(reinterpret_cast<const double2*>(hp + o));
+    const double2 fv = __ldg(reinterpret_cast<const double2*>(fp + o));
+    double f0, f1;
+    fk_pair<DK>(fx, H, W, i, j, a.dn, s_taps, f0, f1);
+    acc[0] = fma(xv.x, xv.x - f0, acc[0]);
+    acc[0] = fma(xv.y, xv.y - f1, acc[0]);
+    acc[1] = fma(xv.x, hv.x, acc[1]);
+    acc[1] = fma(xv.y, hv.y, acc[1]);
+    acc[2] = fma(xv.x, fv.x - xv.x, acc[2]);
+    acc[2] = fma(xv.y, fv.y - xv.y, acc[2]);
+    if (rp) {
+      const double2 rv = __ldg(reinterpret_cast<const double2*>(rp + o));
+      const double d0 = xv.x - rv.x, d1 = xv.y - rv.y;
+      acc[3] = fma(d0, d0, acc[3]);
+      acc[3] = fma(d1, d1, acc[3]);
+    }
+    i += di;
+    j2 += dj;
+    if (j2 >= W2) {
+      j2 -= W2;
+      ++i;
+    }
+  }
+  block_sum<4>(acc, s_red);
+  if (threadIdx.x == 0) {
+    double* dst = a.partials + ((long long)b * nblk + blockIdx.x) * 4;
+    for (int i = 0; i < 4; ++i) dst[i] = acc[i];
+  }
+  __shared__ int s_last;
+  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+    double T[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int blk = 0; blk < nblk; ++blk) {
+      const volatile double* src = a.partials + ((long long)b * nblk + blk) * 4;
+      for (int i = 0; i < 4; ++i) T[i] += src[i];
+    }
+    const double s2 = a.sigma * a.sigma;
+    const double fid = a.yy[b] + s2 * (a.alpha * T[2] - T[1]);
+    if (a.mode == COST_VALUE) {
+      a.out_vals[b * 3 + 0] = fid;
+      a.out_vals[b * 3 + 1] = T[0];
+      a.out_vals[b * 3 + 2] = T[3];
+    } else {
+      cost_finish(st, b, fid, T[0], T[3], a.ref != nullptr, a);
+    }
+    if (a.mode == COST_RECORD) commit_step(st, a.ctl.phase);
+  }
+}
+
+template <int DK>
+static void cost_fp_t(const CostArgs& a, cudaStream_t s) {
+  dim3 grid(cost_fp_chunks(a.B, (long long)a.H * a.W), a.B);
+  k_cost_fp<DK><<<grid, 256, 0, s>>>(a);
+}
+
+void launch_cost_fp(const CostArgs& a, int npairs, cudaStream_t s) {
+  (void)npairs;
+  switch (a.dn.kind) {
+    case DN_CONV: cost_fp_t<DN_CONV>(a, s); break;
+    case DN_MEDIAN3: cost_fp_t<DN_MEDIAN3>(a, s); break;
+    case DN_EXTERNAL: cost_fp_t<DN_EXTERNAL>(a, s); break;
+    default: cost_fp_t<DN_IDENTITY>(a, s); break;
+  }
+}
+
 }  // namespace redve

@@ -152,6 +152,17 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   for (int j = 0; j < 16; ++j)
     if (c0 + j < W) st_cd(s_work + lay.at(line, c0 + j), f[j]);
   __syncthreads();
+  if (a.fout) {  // keep f(x) for the cost identity of this step (cadence only), coalesced
+    const long long N = (long long)H * W;
+    const int nl = min(a.lpc, H - r0);
+    for (int idx = threadIdx.x; idx < nl * W; idx += blockDim.x) {
+      const int l = idx / W, c = idx - l * W;
+      const cd fv = ld_cd(s_work + lay.at(l, c));
+      const long long o = (long long)(r0 + l) * W + c;
+      if (a0) a.fout[(long long)b0 * N + o] = fv.x;
+      if (a1) a.fout[(long long)b1 * N + o] = fv.y;
+    }
+  }
   cd v[16];
   if constexpr (LW > 0) {
     line_fft_ct<LW, false, true>(v, s_work, s_tw, t, line, lay);

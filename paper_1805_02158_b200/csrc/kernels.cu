@@ -258,6 +258,19 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
   }
 }
 int cost_rows(int H) { return H < 8 ? H : 8; }
+
+// out[b] = ||y_b||^2, one CTA per image, fixed reduction order
+__global__ void __launch_bounds__(256) k_sumsq(const double* y, long long n, double* out) {
+  const double* yb = y + (long long)blockIdx.x * n;
+  double acc[1] = {0.0};
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) acc[0] = fma(yb[i], yb[i], acc[0]);
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc[0];
+}
+void launch_sumsq(const double* y, long long n, int B, double* out, cudaStream_t s) {
+  k_sumsq<<<B, 256, 0, s>>>(y, n, out);
+}
 template <int DK>
 static void cost_t(const CostArgs& a, int npairs, cudaStream_t s) {
   static bool done = false;

@@ -17,6 +17,7 @@ struct RowFwdArgs {
   const cd* tws;  // stage-major table (compile-time plans), tw_stage_size(L)
   const ImgState* st;
   int phase;
+  double* fout;  // optional [B][N]: f(x) as computed (cost identity on cadence steps)
 };
 
 struct ColArgs {
@@ -70,6 +71,10 @@ struct CostArgs {
   TraceBufs tr;
   double* partials;
   unsigned* counters;
+  // Fourier-route identity (cost_fp): f(x_prev) of the step, H^T y / sigma^2, ||y||^2
+  const double* fprev;
+  const double* hty;
+  const double* yy;
 };
 
 __device__ inline double psnr_from(double ssd, long long n) {
@@ -147,9 +152,13 @@ void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s);
 void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
 void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);
 int cost_rows(int H);
+int cost_fp_rows(int W);
+void launch_sumsq(const double* y, long long n, int B, double* out, cudaStream_t s);
 void launch_cost(const CostArgs& a, int npairs, cudaStream_t s);
 bool cost_fast_ok(const CostArgs& a);
 void launch_cost_fast(const CostArgs& a, int npairs, cudaStream_t s);
+bool cost_fp_ok(const CostArgs& a);
+void launch_cost_fp(const CostArgs& a, int npairs, cudaStream_t s);
 void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
                       cudaStream_t s);
 void launch_gram(const VeArgs& a, cudaStream_t s);
