@@ -141,8 +141,23 @@ def _oracle_solve(args):
 
 
 def _single_thread_env():
+    """One BLAS thread per process (numpy is already imported, so the pools are
+    limited at run time, not by the environment alone)."""
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def cpu_baseline(cfg_id, n_images, iters_per_solve=BUDGET):
@@ -192,7 +207,7 @@ def run_reference(a):
     import multiprocessing as mp
 
     c = CONFIGS[a.config]
-    cores = os.cpu_count() or 1
+    cores = _host_cores()
     if a.config == 4:  # one huge image: the CPU path is a single process
         cpu = cpu_baseline_spatial()
         line = {"impl": "reference", "metric": SPATIAL_METRIC, "value": cpu["value"],
@@ -213,7 +228,7 @@ def run_reference(a):
         work = [(a.config, i, BUDGET) for i in range(cores)]
         ctx = mp.get_context("fork")
         times = []
-        with ctx.Pool(cores) as pool:
+        with ctx.Pool(cores, initializer=_single_thread_env) as pool:
             for it in range(a.warmup + a.steps):
                 t0 = time.perf_counter()
                 pool.map(_oracle_solve, work, chunksize=1)
@@ -304,6 +319,22 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
         "window_combine": (kp1 + 1) * B * N * s,
     }
     return table.get(kind)
+
+
+def algorithmic_flops(kind, B, N, nf=8, fs=5):
+    """fp64 flops per launch of the compute-bound kernels (FMA = 2 flops)."""
+    if kind == "filter_bank":  # nf correlations + nf adjoint convolutions of fs x fs per pixel
+        return B * N * nf * fs * fs * 2 * 2
+    return None
+
+
+def fp64_peak():
+    p = os.path.join(REPO, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["fp64_fma_tflops"]), \
+                "measured (profiles/fp64_peak.json: tools/fp64_peak.cu FMA chains on this B200 pool)"
+    return 37.2, "nominal 148 SMs x 64 FP64 FMA/clk x 1.965 GHz"
 
 
 def measured_peak():
@@ -404,13 +435,23 @@ def run_native(a):
     step_kernel_ms = sum(v["total_ms"] for v in kernels.values())
     dom = max((k for k in kernels if kernels[k]["gbs"] is not None),
               key=lambda k: kernels[k]["total_ms"])
-    peak, peak_src = measured_peak()
-    ach = kernels[dom]["gbs"]
-    roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": None if ach is None else ach / peak, "peak_source": peak_src,
-            "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
-            "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
-            "traffic": ncu_traffic(dom) if a.config == 1 else None}
+    fl = algorithmic_flops(dom, B, N)
+    if fl is not None:  # compute-bound stencil: fp64 FMA roofline
+        tfs = fl / (kernels[dom]["avg_us"] * 1e-6) / 1e12
+        kernels[dom]["tflops"] = tfs
+        peak, peak_src = fp64_peak()
+        roof = {"bound": "fp64", "kernel": dom, "achieved": tfs, "peak": peak, "unit": "TFLOP/s",
+                "frac": tfs / peak, "peak_source": peak_src,
+                "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
+                "algorithmic_flops_per_launch": fl, "traffic": None}
+    else:
+        peak, peak_src = measured_peak()
+        ach = kernels[dom]["gbs"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": None if ach is None else ach / peak, "peak_source": peak_src,
+                "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
+                "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
+                "traffic": ncu_traffic(dom) if a.config == 1 else None}
 
     # ---- e2e through the public API with host buffers (pinned, allocated up front):
     # problem setup from the host measurements, H2D of y and x0, the solve, D2H of
