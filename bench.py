@@ -262,6 +262,8 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("REDVE_BENCH_NO_SMI") == "1":  # diagnostics only
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",

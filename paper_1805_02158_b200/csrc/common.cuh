@@ -82,6 +82,20 @@ __device__ __forceinline__ bool last_block_of_group(unsigned int* counter, unsig
   return last;
 }
 
+// Sum of the NV partials of nblk CTAs ([nblk][NV] at part) by the whole last
+// CTA: lane-strided L2 loads, then the fixed block_sum tree (deterministic).
+// Result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void gather_partials(const double* part, int nblk, double (&tot)[NV],
+                                                double* smem_red /* >= 32*NV */) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) tot[i] = 0.0;
+  for (int blk = threadIdx.x; blk < nblk; blk += blockDim.x)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tot[i] += __ldcg(part + (long long)blk * NV + i);
+  block_sum<NV>(tot, smem_red);
+}
+
 __device__ __forceinline__ bool finite_d(double v) { return isfinite(v); }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -175,12 +175,10 @@ __global__ void __launch_bounds__(256) k_cost_fast(CostArgs a) {
     for (int i = 0; i < 6; ++i) dst[i] = acc[i];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
-      for (int i = 0; i < 6; ++i) tot[i] += src[i];
-    }
+  const bool lastb = last_block_of_group(a.counters + p, nblk, &s_last);
+  double tot[6];
+  if (lastb) gather_partials<6>(a.partials + (long long)p * nblk * 6, nblk, tot, s_red);
+  if (lastb && threadIdx.x == 0) {
     if (a.mode == COST_VALUE) {
       for (int i = 0; i < 3; ++i) {
         a.out_vals[b0 * 3 + i] = tot[i];
@@ -363,12 +361,10 @@ __global__ void __launch_bounds__(256) k_cost_fp(CostArgs a) {
     for (int i = 0; i < 4; ++i) dst[i] = acc[i];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
-    double T[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)b * nblk + blk) * 4;
-      for (int i = 0; i < 4; ++i) T[i] += src[i];
-    }
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double T[4];
+  if (lastb) gather_partials<4>(a.partials + (long long)b * nblk * 4, nblk, T, s_red);
+  if (lastb && threadIdx.x == 0) {
     const double s2 = a.sigma * a.sigma;
     const double fid = a.yy[b] + s2 * (a.alpha * T[2] - T[1]);
     if (a.mode == COST_VALUE) {

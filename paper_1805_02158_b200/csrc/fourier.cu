@@ -394,12 +394,10 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
     for (int i = 0; i < 6; ++i) dst[i] = acc[i];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
-      for (int i = 0; i < 6; ++i) tot[i] += src[i];
-    }
+  const bool lastb = last_block_of_group(a.counters + p, nblk, &s_last);
+  double tot[6];
+  if (lastb) gather_partials<6>(a.partials + (long long)p * nblk * 6, nblk, tot, s_red);
+  if (lastb && threadIdx.x == 0) {
     if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
     if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
   }

@@ -236,12 +236,10 @@ __global__ void __launch_bounds__(256) k_cost(CostArgs a) {
     for (int i = 0; i < 6; ++i) dst[i] = acc[i];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + p, nblk, &s_last) && threadIdx.x == 0) {
-    double tot[6] = {0, 0, 0, 0, 0, 0};
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)p * nblk + blk) * 6;
-      for (int i = 0; i < 6; ++i) tot[i] += src[i];
-    }
+  const bool lastb = last_block_of_group(a.counters + p, nblk, &s_last);
+  double tot[6];
+  if (lastb) gather_partials<6>(a.partials + (long long)p * nblk * 6, nblk, tot, s_red);
+  if (lastb && threadIdx.x == 0) {
     if (a.mode == COST_VALUE) {
       for (int i = 0; i < 3; ++i) {
         a.out_vals[b0 * 3 + i] = tot[i];
@@ -419,14 +417,11 @@ __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
     for (int i = 0; i < NG; ++i) dst[i] = acc[i];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double tot[NG];
+  if (lastb) gather_partials<NG>(a.partials + (long long)b * nblk * NG, nblk, tot, s_red);
+  if (lastb && threadIdx.x == 0) {
     double G[KP1 * KP1];
-    double tot[NG];
-    for (int i = 0; i < NG; ++i) tot[i] = 0.0;
-    for (int blk = 0; blk < nblk; ++blk) {
-      const volatile double* src = a.partials + ((long long)b * nblk + blk) * NG;
-      for (int i = 0; i < NG; ++i) tot[i] += src[i];
-    }
     int q = 0;
     for (int i = 0; i < KP1; ++i)
       for (int j = i; j < KP1; ++j) {
@@ -642,10 +637,11 @@ __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   const int nblk = gridDim.x;
   if (threadIdx.x == 0) a.partials[(long long)b * nblk + blockIdx.x] = nf[0];
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int blk = 0; blk < nblk; ++blk)
-      tot += ((volatile double*)a.partials)[(long long)b * nblk + blk];
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double tot1[1];
+  if (lastb) gather_partials<1>(a.partials + (long long)b * nblk, nblk, tot1, s_red);
+  if (lastb && threadIdx.x == 0) {
+    const double tot = tot1[0];
     if (tot == 0.0) {
       s.cur = s.start;
       const TraceBufs& tr = a.tr;

@@ -537,12 +537,11 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
     a.partials[((long long)b * nblk + blk) * 2 + 1] = acc[1];
   }
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int i = 0; i < nblk; ++i) {
-      t0 += ((volatile double*)a.partials)[((long long)b * nblk + i) * 2];
-      t1 += ((volatile double*)a.partials)[((long long)b * nblk + i) * 2 + 1];
-    }
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double tt[2];
+  if (lastb) gather_partials<2>(a.partials + (long long)b * nblk * 2, nblk, tt, red);
+  if (lastb && threadIdx.x == 0) {
+    const double t0 = tt[0], t1 = tt[1];
     if (MODE == CG_ITER) {
       cs.alpha = cs.rho / t0;  // rho_cur / (p . q)
     } else if (MODE == CG_INIT) {
@@ -586,9 +585,11 @@ __global__ void __launch_bounds__(256) k_cg_update(CgArgs a) {
   const int nblk = gridDim.x;
   if (threadIdx.x == 0) a.partials[(long long)b * nblk + blockIdx.x] = acc[0];
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
-    double rho = 0.0;
-    for (int i = 0; i < nblk; ++i) rho += ((volatile double*)a.partials)[(long long)b * nblk + i];
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double rr1[1];
+  if (lastb) gather_partials<1>(a.partials + (long long)b * nblk, nblk, rr1, red);
+  if (lastb && threadIdx.x == 0) {
+    const double rho = rr1[0];
     const double rho_prev = cs.rho;
     cs.its += 1;
     if (cs.its >= a.maxiter) {  // loop exhausted: info = maxiter, no final test
@@ -711,10 +712,10 @@ __global__ void __launch_bounds__(256) k_step_record(RecordArgs a) {
   if (threadIdx.x == 0)
     for (int i = 0; i < 3; ++i) a.partials[((long long)b * nblk + blockIdx.x) * 3 + i] = acc[i];
   __shared__ int s_last;
-  if (last_block_of_group(a.counters + b, nblk, &s_last) && threadIdx.x == 0) {
-    double t[3] = {0, 0, 0};
-    for (int i = 0; i < nblk; ++i)
-      for (int j = 0; j < 3; ++j) t[j] += ((volatile double*)a.partials)[((long long)b * nblk + i) * 3 + j];
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double t[3];
+  if (lastb) gather_partials<3>(a.partials + (long long)b * nblk * 3, nblk, t, red);
+  if (lastb && threadIdx.x == 0) {
     record_step(a.st[b], b, t[0], t[1], t[2], a.S, a.ctl, a.tr);
   }
 }
