@@ -965,8 +965,13 @@ int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* c
 
 // CTAs per image for the VE passes (k_gram / k_combine, 256 threads, 2 resident
 // per SM): minimise waves x (pixels per thread + the per-CTA reduction cost),
-// so small batches still fill the GPU and large ones are not cut into slivers.
+// so small batches still fill the GPU and large ones are not cut into slivers
+// (configs[1] sweep: 4 CTAs/image -> gram 60 us, 9 -> 67, 32 -> 80).
 static int ve_chunks(int B, long long N) {
+  if (const char* e = getenv("REDVE_VE_CHUNKS")) {  // experiments
+    const int c = atoi(e);
+    if (c >= 1 && c <= 64) return c;
+  }
   const long long resident = 2LL * 148;
   int best = 1;
   double best_cost = 1e300;
@@ -974,7 +979,7 @@ static int ve_chunks(int B, long long N) {
     if ((long long)c * 256 > N && c > 1) break;
     const long long ctas = (long long)B * c;
     const double waves = (double)((ctas + resident - 1) / resident);
-    const double cost = waves * ((double)N / (256.0 * c) + 6.0);
+    const double cost = waves * ((double)N / (256.0 * c) + 24.0);  // 24: measured tail cost
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = c;

@@ -82,6 +82,8 @@ __device__ __forceinline__ int colwrap(int c, int W) {
   else return wrap(c, W);
 }
 
+constexpr int RF_BATCH = 10;
+
 template <int LW, int DK>
 __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
@@ -110,11 +112,12 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   if ((W & 1) == 0) {  // even width: every row (and image) starts 16-byte aligned
     const int W2 = W >> 1;
     const int total = trows * W2;
-    // batches of 4 iterations: the 8 loads of a batch issue before its stores
-    for (int base = 0; base < total; base += 4 * blockDim.x) {
-      double2 u0[4], u1[4];
+    // batches of RF_BATCH iterations: all loads of a batch issue before its stores
+    // (the tile load is the kernel's exposed latency: keep many in flight)
+    for (int base = 0; base < total; base += RF_BATCH * blockDim.x) {
+      double2 u0[RF_BATCH], u1[RF_BATCH];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < RF_BATCH; ++q) {
         const int idx = base + q * blockDim.x + threadIdx.x;
         const int i = idx / W2, c2 = idx - i * W2;
         const long long o = (long long)wrap(r0 - R + i, H) * W + 2 * c2;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
         u1[q] = (in && x1) ? __ldg(reinterpret_cast<const double2*>(x1 + o)) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < RF_BATCH; ++q) {
         const int idx = base + q * blockDim.x + threadIdx.x;
         if (idx >= total) break;
         const int i = idx / W2, c2 = idx - i * W2;
@@ -344,13 +347,14 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
     const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) + (long long)row * W : nullptr;
     const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N + (long long)row * W : nullptr;
     const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N + (long long)row * W : nullptr;
-    // two batches of 8 columns: all loads of a batch issue before its stores
+    // four batches of 4 columns: all loads of a batch issue before its stores
+    // (8-column batches spilled at the 128-register cap)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double lb0[8], lb1[8], lp0[8], lp1[8];
+    for (int h = 0; h < 4; ++h) {
+      double lb0[4], lb1[4], lp0[4], lp1[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int c = t + T * (8 * h + q);
+      for (int q = 0; q < 4; ++q) {
+        const int c = t + T * (4 * h + q);
         const bool in = c < W;
         lb0[q] = (in && bs0) ? __ldg(bs0 + c) : 0.0;
         lb1[q] = (in && bs1) ? __ldg(bs1 + c) : 0.0;
@@ -358,8 +362,8 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
         lp1[q] = (in && p1) ? __ldg(p1 + c) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int m = 8 * h + q;
+      for (int q = 0; q < 4; ++q) {
+        const int m = 4 * h + q;
         const int c = t + T * m;
         if (c >= W) continue;
         if (o0) {
