@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 #include "rd.cuh"
 #include "slab.cuh"
+#include "fused.cuh"
 #include "sr.cuh"
 
 using namespace redve;
@@ -1095,6 +1096,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     // precomputed denoisers f(x_k) evaluated here is handed to the next step
     // when nothing changes the iterate in between (f_ready).
     const bool ident = p->fourier;
+    const bool fused = p->fourier && !pw && fused_step_ok(p->H, p->W, dn);
     double* f_step = p->fbuf.as<double>();   // f of the current step's input
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
     bool f_ready = false;
@@ -1139,7 +1141,17 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       c.phase = phase;
       c.defer_commit = cadence ? 1 : 0;
       int r = REDVE_OK;
-      if (p->fourier) {
+      if (p->fourier && fused) {  // one clustered kernel per step (fused.cu)
+        FusedArgs fa;
+        memset(&fa, 0, sizeof(fa));
+        fa.B = B; fa.xin = cur; fa.dn = dn; fa.fout = cadence ? p->fprev.as<double>() : nullptr;
+        fa.tws = p->twsW; fa.g = p->g.as<double>(); fa.scale = p->alpha;
+        fa.out = nxt; fa.base = p->xb.as<double>(); fa.xprev = cur; fa.S = S;
+        fa.st = st; fa.ctl = c; fa.tr = tr;
+        fa.partials = p->partials.as<double>(); fa.counters = p->cnt_inv.as<unsigned>();
+        RUN(ctx, "fused_step", launch_fused_step(fa, p->npairs, s));
+        CKL();
+      } else if (p->fourier) {
         {
           View xin = cur;
           DenoiseArgs d = dn;
