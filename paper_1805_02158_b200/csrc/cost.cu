@@ -252,52 +252,6 @@ static int cost_fp_chunks(int B, long long N) {
 }
 
 template <int DK>
-__device__ __forceinline__ void fk_pair(const double* x, int H, int W, int i, int j,
-                                        const DenoiseArgs& dn, const double* taps,
-                                        double& f0, double& f1) {
-  if (DK == DN_MEDIAN3) {
-    const int im = wrap_fast(i - 1, H), ip = wrap_fast(i + 1, H);
-    const int jm = edge_wrap(j - 1, W), jp = edge_wrap(j + 2, W);
-    const double* r0 = x + (long long)im * W;
-    const double* r1 = x + (long long)i * W;
-    const double* r2 = x + (long long)ip * W;
-    double c[4][3];
-    const int cols[4] = {jm, j, j + 1, jp};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double a = __ldg(r0 + cols[q]), b = __ldg(r1 + cols[q]), e = __ldg(r2 + cols[q]);
-      sort2(a, b);
-      sort2(b, e);
-      sort2(a, b);
-      c[q][0] = a;
-      c[q][1] = b;
-      c[q][2] = e;
-    }
-    f0 = med3d(dmax(dmax(c[0][0], c[1][0]), c[2][0]), med3d(c[0][1], c[1][1], c[2][1]),
-               dmin(dmin(c[0][2], c[1][2]), c[2][2]));
-    f1 = med3d(dmax(dmax(c[1][0], c[2][0]), c[3][0]), med3d(c[1][1], c[2][1], c[3][1]),
-               dmin(dmin(c[1][2], c[2][2]), c[3][2]));
-  } else if (DK == DN_CONV) {
-    const int k = dn.ksize, r = k >> 1;
-    double a0 = 0.0, a1 = 0.0;
-    for (int ta = 0; ta < k; ++ta) {
-      const double* row = x + (long long)wrap_fast(i - (ta - r), H) * W;
-      for (int tb = 0; tb < k; ++tb) {
-        const double w = taps[ta * k + tb];
-        a0 = fma(w, __ldg(row + wrap_fast(j - (tb - r), W)), a0);
-        a1 = fma(w, __ldg(row + wrap_fast(j + 1 - (tb - r), W)), a1);
-      }
-    }
-    f0 = a0;
-    f1 = a1;
-  } else {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(x + (long long)i * W + j));
-    f0 = v.x;
-    f1 = v.y;
-  }
-}
-
-template <int DK>
 __global__ void __launch_bounds__(256) k_cost_fp(CostArgs a) {
   const int b = blockIdx.y;
   ImgState& st = a.st[b];

@@ -87,4 +87,74 @@ __device__ __forceinline__ void denoise_span(cd (&f)[16], const cd* tile, const 
   }
 }
 
+// f(x) at the pixel pair (i, j), (i, j+1) of one image from L1-resident
+// neighbours (periodic): the streaming kernels' denoiser (cost.cu k_cost_fp,
+// kernels.cu k_median3_pairs).
+template <int DK>
+__device__ __forceinline__ void fk_pair(const double* x, int H, int W, int i, int j,
+                                        const DenoiseArgs& dn, const double* taps,
+                                        double& f0, double& f1) {
+  if (DK == DN_MEDIAN3) {
+    const int im = wrap_fast(i - 1, H), ip = wrap_fast(i + 1, H);
+    const int jm = edge_wrap(j - 1, W), jp = edge_wrap(j + 2, W);
+    const double* r0 = x + (long long)im * W;
+    const double* r1 = x + (long long)i * W;
+    const double* r2 = x + (long long)ip * W;
+    double c[4][3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cq = q == 0 ? jm : (q == 3 ? jp : j + q - 1);
+      double a = __ldg(r0 + cq), b = __ldg(r1 + cq), e = __ldg(r2 + cq);
+      sort2(a, b);
+      sort2(b, e);
+      sort2(a, b);
+      c[q][0] = a;
+      c[q][1] = b;
+      c[q][2] = e;
+    }
+    f0 = med3d(dmax(dmax(c[0][0], c[1][0]), c[2][0]), med3d(c[0][1], c[1][1], c[2][1]),
+               dmin(dmin(c[0][2], c[1][2]), c[2][2]));
+    f1 = med3d(dmax(dmax(c[1][0], c[2][0]), c[3][0]), med3d(c[1][1], c[2][1], c[3][1]),
+               dmin(dmin(c[1][2], c[2][2]), c[3][2]));
+  } else if (DK == DN_CONV) {
+    const int k = dn.ksize, r = k >> 1;
+    double a0 = 0.0, a1 = 0.0;
+    for (int ta = 0; ta < k; ++ta) {
+      const double* row = x + (long long)wrap_fast(i - (ta - r), H) * W;
+      for (int tb = 0; tb < k; ++tb) {
+        const double w = taps[ta * k + tb];
+        a0 = fma(w, __ldg(row + wrap_fast(j - (tb - r), W)), a0);
+        a1 = fma(w, __ldg(row + wrap_fast(j + 1 - (tb - r), W)), a1);
+      }
+    }
+    f0 = a0;
+    f1 = a1;
+  } else {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(x + (long long)i * W + j));
+    f0 = v.x;
+    f1 = v.y;
+  }
+}
+
+// Periodic k x k correlation (corr) or convolution at the pixel pair
+// (i, j), (i, j+1): out = sum_ab taps[a][b] x(i +- (a-r), j +- (b-r)).
+__device__ __forceinline__ void stencil_pair(const double* x, int H, int W, int i, int j,
+                                             const double* taps, int k, int corr,
+                                             double& f0, double& f1) {
+  const int r = k >> 1;
+  double a0 = 0.0, a1 = 0.0;
+  for (int ta = 0; ta < k; ++ta) {
+    const int da = corr ? (ta - r) : (r - ta);
+    const double* row = x + (long long)wrap_fast(i + da, H) * W;
+    for (int tb = 0; tb < k; ++tb) {
+      const int db = corr ? (tb - r) : (r - tb);
+      const double w = taps[ta * k + tb];
+      a0 = fma(w, __ldg(row + wrap_fast(j + db, W)), a0);
+      a1 = fma(w, __ldg(row + wrap_fast(j + 1 + db, W)), a1);
+    }
+  }
+  f0 = a0;
+  f1 = a1;
+}
+
 }  // namespace redve

@@ -15,6 +15,7 @@
 // CTA of the image (atomic ticket) sums them in CTA order.
 #include <cstdio>
 
+#include "cost.cuh"
 #include "kernels.cuh"
 
 namespace redve {
@@ -668,6 +669,138 @@ void launch_combine(const VeArgs& a, cudaStream_t s) {
   k_combine<<<dim3(a.chunks, a.B), 256, 0, s>>>(a);
 }
 
+// Pair-per-thread streaming stencils (even W): the (row, pair) position is
+// advanced incrementally, neighbours come from L1, 16-byte stores.
+static int pair_chunks(int B, long long N) {
+  int c = (int)((1184 + B - 1) / B);
+  const long long per = (N / 2 + 255) / 256;
+  if (c > per) c = (int)per;
+  if (c > 1024) c = 1024;
+  return c < 1 ? 1 : c;
+}
+
+template <int MODE>  // 0: 3x3 median, 1: k x k stencil (corr / conv, scaled)
+__global__ void __launch_bounds__(256) k_pairs(const double* x, double* out, int H, int W,
+                                               const double* taps, int k, int corr,
+                                               double scale) {
+  const long long N = (long long)H * W;
+  const int b = blockIdx.y;
+  const double* xb = x + (long long)b * N;
+  double* ob = out + (long long)b * N;
+  const int W2 = W >> 1;
+  const long long P = N >> 1;
+  const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int di = (int)(stride / W2), dj = (int)(stride % W2);
+  int i = (int)(q0 / W2), j2 = (int)(q0 % W2);
+  DenoiseArgs dn{DN_MEDIAN3, 0, 1, nullptr};
+  for (long long q = q0; q < P; q += stride) {
+    const int j = 2 * j2;
+    double f0, f1;
+    if (MODE == 0) {
+      fk_pair<DN_MEDIAN3>(xb, H, W, i, j, dn, nullptr, f0, f1);
+    } else {
+      stencil_pair(xb, H, W, i, j, taps, k, corr, f0, f1);
+      f0 *= scale;
+      f1 *= scale;
+    }
+    *reinterpret_cast<double2*>(ob + (long long)i * W + j) = make_double2(f0, f1);
+    i += di;
+    j2 += dj;
+    if (j2 >= W2) {
+      j2 -= W2;
+      ++i;
+    }
+  }
+}
+
+// Eight outputs per thread along a row (W % 8 == 0): each tap row is read once
+// as a register window of 8 + K - 1 values (L1/L2), the 8 accumulators share
+// it, the stores are 16-byte.  Same taps and summation order as k_conv, so
+// results are identical; the median shares sorted columns across the 8.
+static int seg_chunks(int B, long long segs) {
+  int c = (int)((1184 + B - 1) / B);
+  const long long per = (segs + 255) / 256;
+  if (c > per) c = (int)per;
+  if (c > 1024) c = 1024;
+  return c < 1 ? 1 : c;
+}
+
+template <int K, int CORR>
+__global__ void __launch_bounds__(256) k_stencil8(const double* x, double* out, int H, int W,
+                                                  const double* taps, double scale) {
+  constexpr int R = K / 2, WIN = 8 + K - 1;
+  __shared__ double s_t[K * K];
+  for (int q = threadIdx.x; q < K * K; q += blockDim.x) s_t[q] = taps[q];
+  __syncthreads();
+  const long long N = (long long)H * W;
+  const int b = blockIdx.y;
+  const double* xb = x + (long long)b * N;
+  double* ob = out + (long long)b * N;
+  const int S8 = W >> 3;
+  const long long P = (long long)H * S8;
+  const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int di = (int)(stride / S8), ds = (int)(stride % S8);
+  int i = (int)(q0 / S8), sg = (int)(q0 % S8);
+  for (long long q = q0; q < P; q += stride) {
+    const int j0 = 8 * sg;
+    const bool inner = j0 - R >= 0 && j0 + 7 + R < W;
+    double acc[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) acc[m] = 0.0;
+#pragma unroll
+    for (int ta = 0; ta < K; ++ta) {
+      const int da = CORR ? (ta - R) : (R - ta);
+      const double* row = xb + (long long)wrap_fast(i + da, H) * W;
+      double w[WIN];
+      if (inner) {
+#pragma unroll
+        for (int u = 0; u < WIN; ++u) w[u] = __ldg(row + j0 - R + u);
+      } else {
+#pragma unroll
+        for (int u = 0; u < WIN; ++u) w[u] = __ldg(row + wrap_fast(j0 - R + u, W));
+      }
+#pragma unroll
+      for (int tb = 0; tb < K; ++tb) {
+        const double t = s_t[ta * K + tb];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[m] = fma(t, w[CORR ? m + tb : m + K - 1 - tb], acc[m]);
+      }
+    }
+    double2* o2 = reinterpret_cast<double2*>(ob + (long long)i * W + j0);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) o2[m] = make_double2(scale * acc[2 * m], scale * acc[2 * m + 1]);
+    i += di;
+    sg += ds;
+    if (sg >= S8) {
+      sg -= S8;
+      ++i;
+    }
+  }
+}
+
+template <int K>
+static bool stencil8_k(const double* x, double* out, int B, int H, int W, const double* taps,
+                       int corr, double scale, cudaStream_t s) {
+  const dim3 grid(seg_chunks(B, (long long)H * (W / 8)), B);
+  if (corr) k_stencil8<K, 1><<<grid, 256, 0, s>>>(x, out, H, W, taps, scale);
+  else k_stencil8<K, 0><<<grid, 256, 0, s>>>(x, out, H, W, taps, scale);
+  return true;
+}
+
+static bool launch_stencil8(const double* x, double* out, int B, int H, int W, const double* taps,
+                            int k, int corr, double scale, cudaStream_t s) {
+  if (W % 8 != 0 || W < 8 + k) return false;
+  switch (k) {
+    case 3: return stencil8_k<3>(x, out, B, H, W, taps, corr, scale, s);
+    case 5: return stencil8_k<5>(x, out, B, H, W, taps, corr, scale, s);
+    case 7: return stencil8_k<7>(x, out, B, H, W, taps, corr, scale, s);
+    case 9: return stencil8_k<9>(x, out, B, H, W, taps, corr, scale, s);
+    default: return false;
+  }
+}
+
 // --------------------------------------------------------------- stencils (operator API)
 // out = scale * (conv or corr)(x, taps), periodic   (imaging.py:132-170)
 __global__ void k_conv(const double* x, double* out, int B, int H, int W, const double* taps,
@@ -693,6 +826,11 @@ __global__ void k_conv(const double* x, double* out, int B, int H, int W, const 
 void launch_conv(const double* x, double* out, int B, int H, int W, const double* taps, int k,
                  int corr, double scale, cudaStream_t s) {
   long long N = (long long)H * W;
+  if (launch_stencil8(x, out, B, H, W, taps, k, corr, scale, s)) return;
+  if ((W & 1) == 0 && W >= 2) {
+    k_pairs<1><<<dim3(pair_chunks(B, N), B), 256, 0, s>>>(x, out, H, W, taps, k, corr, scale);
+    return;
+  }
   int chunks = cdiv(N, 256);
   if (chunks > 1024) chunks = 1024;
   k_conv<<<dim3(chunks, B), 256, 0, s>>>(x, out, B, H, W, taps, k, corr, scale);
@@ -773,6 +911,10 @@ __global__ void k_median3(const double* x, double* out, int B, int H, int W) {
 }
 void launch_median3(const double* x, double* out, int B, int H, int W, cudaStream_t s) {
   long long N = (long long)H * W;
+  if ((W & 1) == 0 && W >= 4) {
+    k_pairs<0><<<dim3(pair_chunks(B, N), B), 256, 0, s>>>(x, out, H, W, nullptr, 3, 0, 1.0);
+    return;
+  }
   int chunks = cdiv(N, 256);
   if (chunks > 1024) chunks = 1024;
   k_median3<<<dim3(chunks, B), 256, 0, s>>>(x, out, B, H, W);
