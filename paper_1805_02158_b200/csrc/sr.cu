@@ -233,26 +233,28 @@ __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
 
 // Balancing sweep / application with compile-time offsets:
 //   S(p) = v(p) + sum_k [ w0_k(p) v(p+o_k) + w0_k(p-o_k) v(p-o_k) ]
-template <int SR>
+template <int SR, int RPT>
 __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din, double* Dout,
                                                     int first, int apply) {
-  constexpr int X = PW_T + 2 * SR, NP = HalfPlane<SR>::NPOS;
+  // tile: 32 columns x TH = 8*RPT rows (RPT rows per thread; fewer for small
+  // images so the grid still fills the GPU)
+  constexpr int X = PW_T + 2 * SR, TH = 8 * RPT, Y = TH + 2 * SR, NP = HalfPlane<SR>::NPOS;
   const int b = blockIdx.z;
   if (!takes_step(a.st[b], a.phase)) return;
   const int H = a.H, W = a.W;
   double* vs = reinterpret_cast<double*>(s_smem);
-  const int i0 = blockIdx.y * PW_T, j0 = blockIdx.x * PW_T;
+  const int i0 = blockIdx.y * TH, j0 = blockIdx.x * PW_T;
   const long long N = (long long)H * W;
   const double* Db = Din + (long long)b * N;
   const double* x = apply ? a.xin.at(b, a.st) : nullptr;
-  for (int idx = threadIdx.x; idx < X * X; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < Y * X; idx += blockDim.x) {
     const int ti = idx / X, tj = idx - ti * X;
     const long long o = (long long)wrap_fast(i0 - SR + ti, H) * W + wrap_fast(j0 - SR + tj, W);
     const double d = first ? 1.0 : __ldg(Db + o);
     vs[idx] = apply ? d * __ldg(x + o) : d;
   }
   __syncthreads();
-  const bool interior = i0 >= SR && j0 >= SR && i0 + PW_T + SR <= H && j0 + PW_T + SR <= W;
+  const bool interior = i0 >= SR && j0 >= SR && i0 + TH + SR <= H && j0 + PW_T + SR <= W;
   const double* w0b = a.w0 + (long long)b * NP * N;
   const int oj = threadIdx.x & (PW_T - 1);
   const int gj = j0 + oj;
@@ -261,11 +263,11 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
   // that the mirrored loads w0_k(p - o_k) touch were fetched a step earlier;
   // the 4 rows of a thread are accumulated together for memory-level parallelism
   const int cj = oj + SR;
-  int gi[PW_ROWS], ci[PW_ROWS];
-  long long o[PW_ROWS];
-  double S[PW_ROWS];
+  int gi[RPT], ci[RPT];
+  long long o[RPT];
+  double S[RPT];
 #pragma unroll
-  for (int m = 0; m < PW_ROWS; ++m) {
+  for (int m = 0; m < RPT; ++m) {
     const int oi = (threadIdx.x >> 5) + 8 * m;
     gi[m] = min(i0 + oi, H - 1);  // rows past the image edge compute a throwaway copy
     ci[m] = gi[m] - i0 + SR;
@@ -278,14 +280,14 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
       const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
       const double* wk = w0b + (long long)k * N;
       const int sh = di * W + dj;
-      double wp[PW_ROWS], wm[PW_ROWS];
+      double wp[RPT], wm[RPT];
 #pragma unroll
-      for (int m = 0; m < PW_ROWS; ++m) {
+      for (int m = 0; m < RPT; ++m) {
         wp[m] = __ldg(wk + o[m]);
         wm[m] = __ldg(wk + o[m] - sh);
       }
 #pragma unroll
-      for (int m = 0; m < PW_ROWS; ++m) {
+      for (int m = 0; m < RPT; ++m) {
         S[m] = fma(wp[m], vs[(ci[m] + di) * X + cj + dj], S[m]);
         S[m] = fma(wm[m], vs[(ci[m] - di) * X + cj - dj], S[m]);
       }
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
       const double* wk = w0b + (long long)k * N;
       const int cm = wrap_fast(gj - dj, W);
 #pragma unroll
-      for (int m = 0; m < PW_ROWS; ++m) {
+      for (int m = 0; m < RPT; ++m) {
         const double wp = __ldg(wk + o[m]);
         const double wm = __ldg(wk + (long long)wrap_fast(gi[m] - di, H) * W + cm);
         S[m] = fma(wp, vs[(ci[m] + di) * X + cj + dj], S[m]);
@@ -306,11 +308,29 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
     }
   }
 #pragma unroll
-  for (int m = 0; m < PW_ROWS; ++m) {
+  for (int m = 0; m < RPT; ++m) {
     if (i0 + (int)(threadIdx.x >> 5) + 8 * m >= H) break;
     const double d = first ? 1.0 : Db[o[m]];
     if (apply) a.out[(long long)b * N + o[m]] = d * S[m];
     else Dout[(long long)b * N + o[m]] = d / sqrt(d * S[m]);
+  }
+}
+
+template <int SR, int RPT>
+static void pw_sweeps_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
+  dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, 8 * RPT), a.B);
+  const size_t sm = sizeof(double) * (PW_T + 2 * SR) * (8 * RPT + 2 * SR);
+  const double* din = a.D0;
+  double* dout = a.D1;
+  for (int it = 0; it < a.iters; ++it) {
+    k_pw_sweep_t<SR, RPT><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    ++*launches;
+    din = dout;
+    dout = (dout == a.D1) ? a.D0 : a.D1;
+  }
+  if (with_apply) {
+    k_pw_sweep_t<SR, RPT><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+    ++*launches;
   }
 }
 
@@ -320,19 +340,13 @@ static void pw_pass_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_
   constexpr int X = PW_T + 2 * (PR + SR);
   k_pw_weights_t<PR, SR><<<grid, 256, sizeof(double) * X * X, s>>>(a);
   ++*launches;
-  const size_t sm = sizeof(double) * (PW_T + 2 * SR) * (PW_T + 2 * SR);
-  const double* din = a.D0;
-  double* dout = a.D1;
-  for (int it = 0; it < a.iters; ++it) {
-    k_pw_sweep_t<SR><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
-    ++*launches;
-    din = dout;
-    dout = (dout == a.D1) ? a.D0 : a.D1;
-  }
-  if (with_apply) {
-    k_pw_sweep_t<SR><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
-    ++*launches;
-  }
+  // rows per thread: 1 measured best at every size (768^2: 0.91 ms vs 1.30 ms
+  // with 4; 4096^2: 14.7 vs 21.8 ms) -- more, smaller CTAs hide the latency
+  int rpt = 1;
+  if (const char* e = getenv("REDVE_PW_RPT")) rpt = atoi(e);  // experiments
+  if (rpt == 4) pw_sweeps_t<SR, 4>(a, s, launches, with_apply);
+  else if (rpt == 2) pw_sweeps_t<SR, 2>(a, s, launches, with_apply);
+  else pw_sweeps_t<SR, 1>(a, s, launches, with_apply);
 }
 
 // true if a specialisation ran; the final D is in D0 if iters is even, else D1
