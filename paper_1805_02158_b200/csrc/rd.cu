@@ -150,6 +150,107 @@ __global__ void __launch_bounds__(256) k_rd_fast(RdArgs a) {
   }
 }
 
+// configs[3] shape of the stage (8 filters of 5x5): taps and scales in
+// constant memory (uniform operands of the FMAs, no shared loads), a 64 x 32
+// output tile, influence strips of 12 rows and adjoint strips of 8 rows so
+// every loaded column value feeds 5 x strip FMAs.
+constexpr int RB_NF = 8, RB_FS = 5, RB_TW = 64, RB_TH = 32, RB_S1 = 12, RB_S2 = 8;
+__constant__ double c_rb_taps[RB_NF * RB_FS * RB_FS];
+
+__global__ void __launch_bounds__(256) k_rd_bank8(RdArgs a) {
+  constexpr int R = RB_FS / 2;
+  constexpr int X = RB_TW + 4 * R, XH = RB_TH + 4 * R;  // x tile
+  constexpr int PW = RB_TW + 2 * R, PH = RB_TH + 2 * R;  // influence tile
+  constexpr int NS1 = PH / RB_S1;                       // 3 strips x 68 columns
+  static_assert(PH % RB_S1 == 0 && RB_TH % RB_S2 == 0, "strip shapes");
+  static_assert((RB_TH / RB_S2) * RB_TW == 256, "one adjoint strip per thread");
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W;
+  __shared__ double s_isc[RB_NF];
+  if (threadIdx.x < RB_NF) s_isc[threadIdx.x] = 1.0 / (a.scales[threadIdx.x] * a.scales[threadIdx.x]);
+  double* xs = reinterpret_cast<double*>(r_smem);
+  double* ph = xs + X * XH;  // [2][PH][PW]
+  const int i0 = blockIdx.y * RB_TH, j0 = blockIdx.x * RB_TW;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < X * XH; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    xs[idx] = __ldg(x + (long long)wrap_fast(i0 - 2 * R + ti, H) * W + wrap_fast(j0 - 2 * R + tj, W));
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const bool p1 = t < NS1 * PW;
+  const int pc = t % PW, pr0 = (t / PW) * RB_S1;
+  const int oc = t & (RB_TW - 1), or0 = (t / RB_TW) * RB_S2;
+  double acc[RB_S2];
+#pragma unroll
+  for (int m = 0; m < RB_S2; ++m) acc[m] = 0.0;
+#pragma unroll
+  for (int f = 0; f < RB_NF; ++f) {
+    double* phb = ph + (f & 1) * PH * PW;
+    if (p1) {
+      double z[RB_S1];
+#pragma unroll
+      for (int m = 0; m < RB_S1; ++m) z[m] = 0.0;
+#pragma unroll
+      for (int tb = 0; tb < RB_FS; ++tb) {
+        double v[RB_S1 + RB_FS - 1];
+#pragma unroll
+        for (int u = 0; u < RB_S1 + RB_FS - 1; ++u) v[u] = xs[(pr0 + u) * X + pc + tb];
+#pragma unroll
+        for (int ta = 0; ta < RB_FS; ++ta) {
+          const double kk = c_rb_taps[(f * RB_FS + ta) * RB_FS + tb];
+#pragma unroll
+          for (int m = 0; m < RB_S1; ++m) z[m] = fma(kk, v[m + ta], z[m]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < RB_S1; ++m)
+        phb[(pr0 + m) * PW + pc] = z[m] / fma(z[m] * z[m], s_isc[f], 1.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int tb = 0; tb < RB_FS; ++tb) {
+      double v[RB_S2 + RB_FS - 1];
+#pragma unroll
+      for (int u = 0; u < RB_S2 + RB_FS - 1; ++u) v[u] = phb[(or0 + u) * PW + oc + 2 * R - tb];
+#pragma unroll
+      for (int ta = 0; ta < RB_FS; ++ta) {
+        const double kk = c_rb_taps[(f * RB_FS + ta) * RB_FS + tb];
+#pragma unroll
+        for (int m = 0; m < RB_S2; ++m) acc[m] = fma(kk, v[m + 2 * R - ta], acc[m]);
+      }
+    }
+  }
+  const long long N = (long long)H * W;
+  const int gj = j0 + oc;
+#pragma unroll
+  for (int m = 0; m < RB_S2; ++m) {
+    const int gi = i0 + or0 + m;
+    if (gi >= H || gj >= W) continue;
+    const double xv = xs[(or0 + m + 2 * R) * X + (oc + 2 * R)];
+    a.out[(long long)b * N + (long long)gi * W + gj] = fma(-a.tau, acc[m], xv);
+  }
+}
+
+static bool launch_rd_bank8(const RdArgs& a, cudaStream_t s) {
+  if (a.nf != RB_NF || a.fs != RB_FS) return false;
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_rd_bank8, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+  }
+  // taps into constant memory (stream-ordered; a memcpy node under graph capture)
+  cudaMemcpyToSymbolAsync(c_rb_taps, a.filters, sizeof(double) * RB_NF * RB_FS * RB_FS, 0,
+                          cudaMemcpyDeviceToDevice, s);
+  constexpr int R = RB_FS / 2;
+  const size_t smem = sizeof(double) * ((size_t)(RB_TW + 4 * R) * (RB_TH + 4 * R) +
+                                        2 * (size_t)(RB_TW + 2 * R) * (RB_TH + 2 * R));
+  dim3 grid((a.W + RB_TW - 1) / RB_TW, (a.H + RB_TH - 1) / RB_TH, a.B);
+  k_rd_bank8<<<grid, 256, smem, s>>>(a);
+  return true;
+}
+
 template <int FS>
 static size_t rd_fast_smem(int nf) {
   constexpr int R = FS / 2, X = RD_T + 4 * R, P = RD_T + 2 * R;
@@ -170,6 +271,7 @@ void launch_rd(const RdArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_rd_fast<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = true;
   }
+  if (launch_rd_bank8(a, s)) return;
   dim3 grid((a.W + RD_T - 1) / RD_T, (a.H + RD_T - 1) / RD_T, a.B);
   switch (a.fs) {
     case 3: k_rd_fast<3><<<grid, 256, rd_fast_smem<3>(a.nf), s>>>(a); return;
