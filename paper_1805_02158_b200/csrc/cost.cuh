@@ -46,6 +46,33 @@ __device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, co
   return r;
 }
 
+// k x k periodic convolution over the 16 contiguous columns [c0, c0+16) of
+// tile row ti (pairs), K known at compile time.  Same terms and per-output
+// order (ta outer, tb inner) as the runtime loop below.
+template <int K, class Wrap>
+__device__ __forceinline__ void conv_span(cd (&f)[16], const cd* tile, const TileLayout& tl, int ti,
+                                          int c0, const double* taps, Wrap wrapc) {
+  constexpr int r = K / 2;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) f[j] = cd{0.0, 0.0};
+#pragma unroll
+  for (int ta = 0; ta < K; ++ta) {
+    cd row[16 + K - 1];  // columns c0 - r .. c0 + 15 + r of tile row ti - (ta - r)
+#pragma unroll
+    for (int u = 0; u < 16 + K - 1; ++u) row[u] = ld_cd(tile + tl.at(ti - (ta - r), wrapc(c0 - r + u)));
+#pragma unroll
+    for (int tb = 0; tb < K; ++tb) {
+      const double w = taps[ta * K + tb];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const cd xx = row[j + K - 1 - tb];  // column c0 + j - (tb - r)
+        f[j].x = fma(w, xx.x, f[j].x);
+        f[j].y = fma(w, xx.y, f[j].y);
+      }
+    }
+  }
+}
+
 // f over the 16 contiguous columns [c0, c0+16) of tile row ti (pairs).
 // WRAP(c) maps a column in [-r, W + r) into [0, W).
 template <int DK, class Wrap>
@@ -66,6 +93,10 @@ __device__ __forceinline__ void denoise_span(cd (&f)[16], const cd* tile, const 
       A = B;
       B = C;
     }
+  } else if (DK == DN_CONV && (ksize == 3 || ksize == 5)) {
+    // compile-time taps loop: the 16 accumulator chains interleave
+    if (ksize == 3) conv_span<3>(f, tile, tl, ti, c0, taps, wrapc);
+    else conv_span<5>(f, tile, tl, ti, c0, taps, wrapc);
   } else if (DK == DN_CONV) {
     const int r = ksize >> 1;
 #pragma unroll
