@@ -567,20 +567,42 @@ __device__ __forceinline__ double combine_span(const VeArgs& a, int b, int s0, d
   for (int j = 0; j < KE; ++j) xi[j] = xi_s[j];
   double nf = 0.0;
   const long long N2 = (a.N & 1) ? 0 : (a.N >> 1);
-#pragma unroll 2
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N2;
-       p += (long long)gridDim.x * blockDim.x) {
-    double2 prev = reinterpret_cast<const double2*>(w[0])[p];
-    double2 acc = prev;
+  // batches of U pixel pairs: every load of a batch is issued before its
+  // stores (out is one of the window slots, so the compiler cannot hoist
+  // loads across the stores by itself)
+  constexpr int U = 4;
+  const long long st = (long long)gridDim.x * blockDim.x;
+  for (long long p0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; p0 < N2; p0 += U * st) {
+    double2 acc[U], prev[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long p = p0 + u * st;
+      prev[u] = p < N2 ? reinterpret_cast<const double2*>(w[0])[p] : make_double2(0.0, 0.0);
+      acc[u] = prev[u];
+    }
 #pragma unroll
     for (int j = 0; j < KE; ++j) {
-      const double2 nx = reinterpret_cast<const double2*>(w[j + 1])[p];
-      acc.x = fma(xi[j], nx.x - prev.x, acc.x);
-      acc.y = fma(xi[j], nx.y - prev.y, acc.y);
-      prev = nx;
+      double2 nx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long p = p0 + u * st;
+        nx[u] = p < N2 ? reinterpret_cast<const double2*>(w[j + 1])[p] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u].x = fma(xi[j], nx[u].x - prev[u].x, acc[u].x);
+        acc[u].y = fma(xi[j], nx[u].y - prev[u].y, acc[u].y);
+        prev[u] = nx[u];
+      }
     }
-    reinterpret_cast<double2*>(out)[p] = acc;
-    nf += (isfinite(acc.x) ? 0.0 : 1.0) + (isfinite(acc.y) ? 0.0 : 1.0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long p = p0 + u * st;
+      if (p < N2) {
+        reinterpret_cast<double2*>(out)[p] = acc[u];
+        nf += (isfinite(acc[u].x) ? 0.0 : 1.0) + (isfinite(acc[u].y) ? 0.0 : 1.0);
+      }
+    }
   }
   for (long long p = 2 * N2 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.N;
        p += (long long)gridDim.x * blockDim.x) {
@@ -598,6 +620,7 @@ __device__ __forceinline__ double combine_span(const VeArgs& a, int b, int s0, d
   return nf;
 }
 
+template <int KP1>
 __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   const int b = blockIdx.y;
   ImgState& s = a.st[b];
@@ -616,24 +639,15 @@ __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   __shared__ double s_xi[MAXKP1];
   __shared__ double s_red[32];
   const int ke = s.ve_k;
-  if (threadIdx.x < ke) s_xi[threadIdx.x] = s.ve_xi[threadIdx.x];
+  // weights past the extrapolation order are zero: the span always walks the
+  // full window (KP1 differences, compile-time) so the kernel's registers are
+  // sized for this configuration, not for the largest kappa
+  if (threadIdx.x < MAXKP1) s_xi[threadIdx.x] = threadIdx.x < ke ? s.ve_xi[threadIdx.x] : 0.0;
   __syncthreads();
   const int s0 = s.start + a.m;
   double* out = a.ring + (long long)b * a.img_stride + (long long)s.start * a.slot_stride;
   double nf[1];
-  switch (ke) {
-    case 1: nf[0] = combine_span<1>(a, b, s0, out, s_xi); break;
-    case 2: nf[0] = combine_span<2>(a, b, s0, out, s_xi); break;
-    case 3: nf[0] = combine_span<3>(a, b, s0, out, s_xi); break;
-    case 4: nf[0] = combine_span<4>(a, b, s0, out, s_xi); break;
-    case 5: nf[0] = combine_span<5>(a, b, s0, out, s_xi); break;
-    case 6: nf[0] = combine_span<6>(a, b, s0, out, s_xi); break;
-    case 7: nf[0] = combine_span<7>(a, b, s0, out, s_xi); break;
-    case 8: nf[0] = combine_span<8>(a, b, s0, out, s_xi); break;
-    case 9: nf[0] = combine_span<9>(a, b, s0, out, s_xi); break;
-    case 10: nf[0] = combine_span<10>(a, b, s0, out, s_xi); break;
-    default: nf[0] = combine_span<11>(a, b, s0, out, s_xi); break;
-  }
+  nf[0] = combine_span<KP1 - 1>(a, b, s0, out, s_xi);  // ke <= kappa = KP1 - 1
   block_sum<1>(nf, s_red);
   const int nblk = gridDim.x;
   if (threadIdx.x == 0) a.partials[(long long)b * nblk + blockIdx.x] = nf[0];
@@ -666,7 +680,15 @@ __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   }
 }
 void launch_combine(const VeArgs& a, cudaStream_t s) {
-  k_combine<<<dim3(a.chunks, a.B), 256, 0, s>>>(a);
+  const dim3 grid(a.chunks, a.B);
+  switch (a.kp1) {
+#define COMBINE_CASE(K) \
+  case K: k_combine<K><<<grid, 256, 0, s>>>(a); break;
+    COMBINE_CASE(2) COMBINE_CASE(3) COMBINE_CASE(4) COMBINE_CASE(5) COMBINE_CASE(6)
+    COMBINE_CASE(7) COMBINE_CASE(8) COMBINE_CASE(9) COMBINE_CASE(10) COMBINE_CASE(11)
+#undef COMBINE_CASE
+    default: k_combine<12><<<grid, 256, 0, s>>>(a); break;
+  }
 }
 
 // Pair-per-thread streaming stencils (even W): the (row, pair) position is
