@@ -455,6 +455,19 @@ def run_native(a):
                 "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
                 "traffic": ncu_traffic(dom) if a.config == 1 else None}
 
+    # whole-step roofline against SURVEY.md 8(d)'s per-iteration algorithmic
+    # bytes for the deblur step, N s (2 + 7.5 + 2 + 1 + (2k+3)/(m+k+1) + 4/c)
+    step_roof = None
+    if c["kind"] == "deblur":
+        cad = 5 if N > 16384 else 1
+        units = 2 + 7.5 + 2 + 1 + (2 * KAPPA + 3) / (0 + KAPPA + 1) + 4 / cad
+        bpi = units * B * N * 8
+        gbs = bpi / (ms / max(iters, 1) * 1e-3) / 1e9
+        hbm = measured_peak()[0]
+        step_roof = {"model": "SURVEY.md 8(d): N*s*(2+7.5+2+1+(2k+3)/(m+k+1)+4/c) per image-iteration",
+                     "units_per_image_iteration": units, "bytes_per_iteration": bpi,
+                     "achieved_gbs": gbs, "peak": hbm, "frac": gbs / hbm}
+
     # ---- e2e through the public API with host buffers (pinned, allocated up front):
     # problem setup from the host measurements, H2D of y and x0, the solve, D2H of
     # the solutions (traces come back inside solve_batch)
@@ -503,6 +516,7 @@ def run_native(a):
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "step_roofline": step_roof,
             "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk,
