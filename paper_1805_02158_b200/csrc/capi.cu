@@ -241,6 +241,7 @@ struct redve_problem {
   // Fourier-route cost identity: f(x_{k-1}) of cadence steps, second f buffer
   // for the precomputed denoisers, ||y||^2 per image
   DevBuf fprev, fcur, yy;
+  DevBuf Z2, fprev2;  // k_row_mid: second spectrum / f(x) buffers (ping-pong)
   bool has_ref = false;
   const cd* twH = nullptr;
   const cd* twW = nullptr;
@@ -860,6 +861,11 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     if (r) return bail(r);
     // cost identity on the Fourier route (cost.cu k_cost_fp)
     PK(p->fprev.ensure(sizeof(double) * p->N * B));
+    if (dn->kind != REDVE_DN_PATCH && dn->kind != REDVE_DN_FILTERBANK &&
+        dn->kind != REDVE_DN_EXTERNAL && row_mid_ok(H, W, dn_args(p), p->lpc_row)) {  // opt-in
+      PK(p->Z2.ensure(sizeof(cd) * p->N * p->npairs));
+      PK(p->fprev2.ensure(sizeof(double) * p->N * B));
+    }
     PK(p->yy.ensure(sizeof(double) * B));
     RUN(ctx, "sumsq", launch_sumsq(p->y.as<double>(), Ny, B, p->yy.as<double>(), s));
     PK(cudaGetLastError());
@@ -1100,7 +1106,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     double* f_step = p->fbuf.as<double>();   // f of the current step's input
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
     bool f_ready = false;
-    auto cost_of_cur = [&](int mode, StepCtl c) -> int {
+    auto cost_of_cur = [&](int mode, StepCtl c, const double* fprev_rec = nullptr) -> int {
       const double* fe = nullptr;
       const int ph = mode == COST_RECORD ? c.phase : PH_SETUP;
       if (pw) {
@@ -1111,7 +1117,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
       CostArgs ca = cost_args(p, cur, fe, mode, c, tr);
       if (ident && mode == COST_RECORD) {
-        ca.fprev = pw ? f_step : p->fprev.as<double>();
+        ca.fprev = pw ? f_step : (fprev_rec ? fprev_rec : p->fprev.as<double>());
         ca.hty = p->hty.as<double>();
         ca.yy = p->yy.as<double>();
       }
@@ -1135,16 +1141,26 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       CKL();
     }
 
-    cd* zc = p->Z.as<cd>();
-    auto step = [&](int phase, bool cadence) -> int {
+    // k_row_mid: the inverse row pass of a step and the forward row pass of the
+    // next step in one kernel, whenever the next step follows directly (inside
+    // a VE cycle / plain FP run; never across an extrapolation)
+    const bool mid = p->fourier && !pw && !fused && p->Z2.p != nullptr &&
+                     row_mid_ok(p->H, p->W, dn, p->lpc_row);
+    cd* zcur = p->Z.as<cd>();
+    cd* zalt = mid ? p->Z2.as<cd>() : nullptr;
+    double* fpb[2] = {p->fprev.as<double>(), mid ? p->fprev2.as<double>() : p->fprev.as<double>()};
+    bool z_ready = false;  // zcur already holds this step's row spectra
+    int kk = 0;            // steps issued so far (f(x) buffer parity)
+    auto step = [&](int phase, bool cadence, bool fuse_next, bool next_cadence) -> int {
       StepCtl c = ctl;
       c.phase = phase;
       c.defer_commit = cadence ? 1 : 0;
       int r = REDVE_OK;
+      double* fp_this = fpb[kk & 1];
       if (p->fourier && fused) {  // one clustered kernel per step (fused.cu)
         FusedArgs fa;
         memset(&fa, 0, sizeof(fa));
-        fa.B = B; fa.xin = cur; fa.dn = dn; fa.fout = cadence ? p->fprev.as<double>() : nullptr;
+        fa.B = B; fa.xin = cur; fa.dn = dn; fa.fout = cadence ? fp_this : nullptr;
         fa.tws = p->twsW; fa.g = p->g.as<double>(); fa.scale = p->alpha;
         fa.out = nxt; fa.base = p->xb.as<double>(); fa.xprev = cur; fa.S = S;
         fa.st = st; fa.ctl = c; fa.tr = tr;
@@ -1165,11 +1181,27 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
             d.radius = 0;
           }
           f_ready = false;
-          double* fout = (cadence && !pw) ? p->fprev.as<double>() : nullptr;
-          if ((r = f_row_fwd(p, xin, d, zc, phase, fout))) return r;
+          double* fout = (cadence && !pw) ? fp_this : nullptr;
+          if (!z_ready && (r = f_row_fwd(p, xin, d, zcur, phase, fout))) return r;
         }
-        if ((r = f_col(p, zc, p->alpha, phase))) return r;
-        r = f_row_inv(p, zc, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
+        if ((r = f_col(p, zcur, p->alpha, phase))) return r;
+        if (mid && fuse_next) {
+          RowMidArgs ma;
+          memset(&ma, 0, sizeof(ma));
+          ma.B = B; ma.H = p->H; ma.W = p->W; ma.lpc = p->lpc_row;
+          ma.Zin = zcur; ma.out = nxt; ma.base = p->xb.as<double>(); ma.xprev = cur; ma.S = S;
+          ma.st = st; ma.ctl = c; ma.tr = tr;
+          ma.partials = p->partials.as<double>(); ma.counters = p->cnt_inv.as<unsigned>();
+          ma.dn = dn; ma.Zout = zalt; ma.fout = next_cadence ? fpb[(kk + 1) & 1] : nullptr;
+          ma.tws = p->twsW;
+          RUN(ctx, "row_mid", launch_row_mid(ma, p->npairs, s));
+          CKL();
+          std::swap(zcur, zalt);
+          z_ready = true;
+        } else {
+          r = f_row_inv(p, zcur, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
+          z_ready = false;
+        }
       } else {
         r = fp_step_cg(p, cur, nxt, phase, nullptr);
         if (r) return r;
@@ -1181,13 +1213,14 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
       if (r) return r;
       if (cadence) {
-        r = cost_of_cur(COST_RECORD, c);
+        r = cost_of_cur(COST_RECORD, c, fp_this);
         if (r) return r;
         if (track) {
           RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
           CKL();
         }
       }
+      ++kk;
       return REDVE_OK;
     };
 
@@ -1204,7 +1237,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     int k = 0;
     if (!ve) {
       while (k < budget) {
-        int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+        int r = step(PH_MAIN, ((k + 1) % log_every) == 0, k + 1 < budget,
+                     ((k + 2) % log_every) == 0);
         if (r) return r;
         ++k;
         if (!use_graph && k % (check_every * clen) == 0 && k < budget) {
@@ -1218,7 +1252,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       while (true) {
         int n = 0;
         for (int i = 0; i < clen; ++i) {
-          int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
+          int r = step(PH_MAIN, ((k + 1) % log_every) == 0, i + 1 < clen && k + 1 < budget,
+                       ((k + 2) % log_every) == 0);
           if (r) return r;
           ++k;
           ++n;
@@ -1242,7 +1277,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
     }
     for (int i = 0; i < stab; ++i) {
-      int r = step(PH_STAB, true);
+      int r = step(PH_STAB, true, i + 1 < stab, true);
       if (r) return r;
     }
     if (track) {  // finalize (solvers.py:255-262)
