@@ -13,7 +13,10 @@ from .denoisers import (BUILTIN_DENOISERS, FilterBank, GaussianFilter, Identity,
 from .errors import (CgNoConvergence, DegenerateSum, InvalidSize, KernelTooLarge, NoConvergence,
                      NonFiniteIterate, RankDeficient, ShapeMismatch, ZeroFirstColumn)
 from .extrapolation import (METHODS, MPE, RRE, SVDMPE, ExtrapolationResult, ExtrapolationWeights,
-                            VectorSequenceWindow, extrapolate_batch, extrapolate_once)
+                            QrFactorization, ReconstructionCoefficients, VectorSequenceWindow,
+                            build_difference_matrix, extrapolate_batch, extrapolate_once,
+                            gamma_mpe, gamma_rre, gamma_svdmpe, mgs_qr, reconstruct,
+                            reconstruction_coefficients, small_svd)
 from .imaging import (Blur, BlurDownsample, Psf, as_image, degrade, gaussian_noise, make_psf, psnr,
                       synthetic_image)
 from .objective import (RedObjective, as_fixed_point_problem, check_local_homogeneity,

@@ -26,7 +26,9 @@ SVDMPE = "svdmpe"
 METHODS = (MPE, RRE, SVDMPE)
 
 __all__ = ["MPE", "RRE", "SVDMPE", "METHODS", "VectorSequenceWindow", "ExtrapolationWeights",
-           "ExtrapolationResult", "ReconstructionCoefficients", "extrapolate_once",
+           "ExtrapolationResult", "ReconstructionCoefficients", "QrFactorization",
+           "build_difference_matrix", "mgs_qr", "small_svd", "gamma_mpe", "gamma_rre",
+           "gamma_svdmpe", "reconstruction_coefficients", "reconstruct", "extrapolate_once",
            "extrapolate_batch", "ZeroFirstColumn", "DegenerateSum", "RankDeficient",
            "NoConvergence"]
 
@@ -97,6 +99,176 @@ class ExtrapolationResult:
     converged: bool
     extrapolated: bool
     kappa_used: int
+
+
+@dataclass(frozen=True)
+class QrFactorization:
+    """Thin QR of the difference matrix (extrapolation.py:97-109).  ``Q`` is
+    an [N, kappa+1] CUDA tensor (a column-major view), ``R`` a host array."""
+
+    Q: object
+    R: np.ndarray
+    effective_rank: int
+    rank_tolerance: float
+
+
+# --------------------------------------------------------------------- factor-level API
+# The pieces extrapolate_once chains together, for callers that use them on
+# their own (extrapolation.py:154-316).  The N-length vector work (differences,
+# Gram-Schmidt projections, reconstruction) runs in libredve_b200's vector
+# primitives; the (kappa+1)^2 triangular algebra is host arithmetic, as in the
+# reference.
+
+
+def _dev_rows(v):
+    t, _ = _io.to_device(v)
+    return t.reshape(t.shape[0], -1).contiguous()
+
+
+def _dot(x, y):
+    out = C.c_double()
+    ctx = nat.context()
+    nat.check(nat.library().redve_vec_dot(ctx, x.numel(), nat.dptr(x), nat.dptr(y), C.byref(out)),
+              ctx)
+    return out.value
+
+
+def _axpby(a, x, b, y):
+    ctx = nat.context()
+    nat.check(nat.library().redve_vec_axpby(ctx, y.numel(), float(a), nat.dptr(x), float(b),
+                                            nat.dptr(y)), ctx)
+
+
+def build_difference_matrix(window: VectorSequenceWindow):
+    """N x (kappa+1) matrix whose column i is x_{m+i+1} - x_{m+i}
+    (extrapolation.py:154-156); a column-major view of a device buffer."""
+    rows = _dev_rows(window.vectors)
+    diff = rows[1:].clone()
+    for i in range(diff.shape[0]):
+        _axpby(-1.0, rows[i], 1.0, diff[i])
+    return diff.T
+
+
+def mgs_qr(u, rank_tolerance: float = 1e-12) -> QrFactorization:
+    """Modified Gram-Schmidt with two projection sweeps per column and the
+    relative rank cut r_ii < tol * r_11 (extrapolation.py:159-196)."""
+    if rank_tolerance <= 0:
+        raise ValueError("rank_tolerance must be positive")
+    t, _ = _io.to_device(u)
+    if t.dim() != 2:
+        raise ValueError("mgs_qr expects an N x k matrix")
+    cols = t.T.contiguous()  # column i contiguous
+    k = cols.shape[0]
+    q = _io.torch_mod().zeros_like(cols)
+    r = np.zeros((k, k))
+    r11 = 0.0
+    effective = k
+    for i in range(k):
+        v = cols[i].clone()
+        for _sweep in range(2):
+            for j in range(i):
+                proj = _dot(q[j], v)
+                r[j, i] += proj
+                _axpby(-proj, q[j], 1.0, v)
+        rii = float(np.sqrt(_dot(v, v)))
+        r[i, i] = rii
+        if i == 0:
+            if rii < 1e-300:
+                raise ZeroFirstColumn("first difference column is zero")
+            r11 = rii
+        elif rii < rank_tolerance * r11:
+            effective = i
+            break
+        _axpby(0.0, v, 1.0 / rii, v)
+        q[i].copy_(v)
+    return QrFactorization(Q=q.T, R=r, effective_rank=effective, rank_tolerance=rank_tolerance)
+
+
+def small_svd(r):
+    """SVD of the small triangular factor (extrapolation.py:199-214)."""
+    r = np.asarray(r, dtype=np.float64)
+    if r.ndim != 2 or r.shape[0] != r.shape[1]:
+        raise ValueError("small_svd expects a square matrix")
+    if r.shape[0] > 64:
+        raise ValueError("small_svd is intended for windows of order <= 63")
+    try:
+        return np.linalg.svd(r)
+    except np.linalg.LinAlgError as exc:  # pragma: no cover - pathological input
+        raise NoConvergence(str(exc)) from exc
+
+
+def _require_full_rank(qr: QrFactorization) -> int:
+    ncols = qr.R.shape[0]
+    if qr.effective_rank != ncols:
+        raise RankDeficient(f"effective rank {qr.effective_rank} < {ncols}; shrink the window order")
+    return ncols - 1
+
+
+def _normalized(method, c, denom):
+    gamma = c / denom
+    return ExtrapolationWeights(method=method, c=c, gamma=gamma,
+                                stability_sum=float(np.abs(gamma).sum()))
+
+
+def _upper_solve(r, b, trans=False):
+    from scipy.linalg import solve_triangular
+
+    return solve_triangular(r, b, trans="T" if trans else "N", lower=False)
+
+
+def gamma_mpe(qr: QrFactorization) -> ExtrapolationWeights:
+    """MPE weights; DegenerateSum when sum(c) vanishes (extrapolation.py:241-260)."""
+    kappa = _require_full_rank(qr)
+    cp = _upper_solve(qr.R[:kappa, :kappa], -qr.R[:kappa, kappa])
+    c = np.append(cp, 1.0)
+    s = float(c.sum())
+    if abs(s) < 1e-12 * float(np.abs(c).sum()) or not np.isfinite(s):
+        raise DegenerateSum("MPE coefficient sum vanished")
+    return _normalized(MPE, c, s)
+
+
+def gamma_rre(qr: QrFactorization) -> ExtrapolationWeights:
+    """RRE weights from (R^T R) d = 1 (extrapolation.py:263-273)."""
+    _require_full_rank(qr)
+    d = _upper_solve(qr.R, _upper_solve(qr.R, np.ones(qr.R.shape[0]), trans=True))
+    return _normalized(RRE, d, float(d.sum()))
+
+
+def gamma_svdmpe(qr: QrFactorization) -> ExtrapolationWeights:
+    """SVD-MPE weights: right singular vector of the smallest singular value
+    (extrapolation.py:276-284)."""
+    _require_full_rank(qr)
+    _, _, vt = small_svd(qr.R)
+    v = vt[-1].copy()
+    s = float(v.sum())
+    if abs(s) < 1e-12 or not np.isfinite(s):
+        raise DegenerateSum("SVD-MPE singular-vector sum vanished")
+    return _normalized(SVDMPE, v, s)
+
+
+def reconstruction_coefficients(gamma, r) -> ReconstructionCoefficients:
+    """xi_j = 1 - (gamma_0 + ... + gamma_j), eta = R xi (extrapolation.py:295-305)."""
+    gamma = np.asarray(gamma, dtype=np.float64)
+    kappa = len(gamma) - 1
+    xi = 1.0 - np.cumsum(gamma[:kappa])
+    eta = np.asarray(r)[:kappa, :kappa] @ xi
+    return ReconstructionCoefficients(xi=xi, eta=eta)
+
+
+def reconstruct(window: VectorSequenceWindow, qr: QrFactorization, w: ExtrapolationWeights):
+    """x_m + Q (R xi) through the factors (extrapolation.py:308-316); a device
+    tensor when the window lives on the device, else a numpy array."""
+    kappa = window.kappa
+    if len(w.gamma) != kappa + 1:
+        raise ValueError(f"{len(w.gamma)} weights for a window of order {kappa}")
+    coeffs = reconstruction_coefficients(w.gamma, qr.R)
+    rows = _dev_rows(window.vectors)
+    out = rows[0].clone()
+    qcols = qr.Q.T if _io.is_tensor(qr.Q) else _dev_rows(np.asarray(qr.Q).T)
+    for j in range(kappa):
+        _axpby(float(coeffs.eta[j]), qcols[j].contiguous(), 1.0, out)
+    out = out.reshape(window.vectors.shape[1:])
+    return out if _io.is_tensor(window.vectors) else out.cpu().numpy()
 
 
 def _weights_from(res: "nat.VeResultC", requested: str):
