@@ -17,7 +17,8 @@ from .extrapolation import (METHODS, MPE, RRE, SVDMPE, ExtrapolationResult, Extr
                             build_difference_matrix, extrapolate_batch, extrapolate_once,
                             gamma_mpe, gamma_rre, gamma_svdmpe, mgs_qr, reconstruct,
                             reconstruction_coefficients, small_svd)
-from .imaging import (Blur, BlurDownsample, Psf, as_image, degrade, gaussian_noise, make_psf, psnr,
+from .imaging import (Blur, BlurDownsample, Psf, as_image, convolve_circular, degrade, dft2,
+                      embed_psf, gaussian_noise, idft2, make_psf, psf_spectrum, psnr,
                       synthetic_image)
 from .objective import (RedObjective, as_fixed_point_problem, check_local_homogeneity,
                         check_passivity, default_step_size)

@@ -76,6 +76,48 @@ def make_psf(kind: str, size: int, std: float | None = None) -> Psf:
     raise InvalidSize(f"unknown PSF kind {kind!r}")
 
 
+# ---------------------------------------------------------------- DFT helpers
+# (imaging.py:100-145).  Host arrays follow numpy's convention exactly, as the
+# reference; device tensors stay on the device (cuFFT through torch) -- these
+# are utilities, the solver's transforms are fourier.cu's fused kernels.
+
+
+def dft2(image):
+    """2-D DFT, numpy "backward" convention (idft2(dft2(x)) == x)."""
+    if _io.is_tensor(image):
+        return _io.torch_mod().fft.fft2(image)
+    return np.fft.fft2(image)
+
+
+def idft2(spectrum):
+    """Inverse of :func:`dft2`; the real part."""
+    if _io.is_tensor(spectrum):
+        return _io.torch_mod().fft.ifft2(spectrum).real
+    return np.fft.ifft2(spectrum).real
+
+
+def embed_psf(psf: "Psf", shape) -> np.ndarray:
+    """The kernel in a full-size array with its anchor at (0, 0)."""
+    h, w = shape
+    if psf.size > min(h, w):
+        raise KernelTooLarge(f"{psf.size}x{psf.size} PSF on a {h}x{w} image")
+    full = np.zeros(shape)
+    full[: psf.size, : psf.size] = psf.taps
+    return np.roll(full, (-psf.radius, -psf.radius), axis=(0, 1))
+
+
+def psf_spectrum(psf: "Psf", shape) -> np.ndarray:
+    """Transfer function of circular convolution with the kernel."""
+    return dft2(embed_psf(psf, shape))
+
+
+def convolve_circular(image, psf: "Psf"):
+    """Circular convolution of an image with a kernel (imaging.py:132-145),
+    computed by the device stencil (same sum as the reference's DFT product)."""
+    shape = tuple(np.shape(image))[-2:]
+    return Blur(psf, shape).apply(image)
+
+
 def _batched(x, shape):
     t, from_np = _io.to_device(x)
     single = t.dim() == 2
@@ -106,6 +148,15 @@ class _Operator:
                      nat.dptr(t), nat.dptr(out)), ctx)
         out = out[0] if single else out
         return _io.to_host(out, from_np)
+
+    @property
+    def spectrum(self) -> np.ndarray:
+        """psf_spectrum of the blur on the input grid (imaging.py:165, 191)."""
+        sp = getattr(self, "_spectrum", None)
+        if sp is None:
+            sp = psf_spectrum(self.psf, self.in_shape)
+            self._spectrum = sp
+        return sp
 
     def apply(self, x):
         return self._run(nat.library().redve_operator_apply, x, self.in_shape, self.out_shape)

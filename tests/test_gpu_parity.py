@@ -80,6 +80,16 @@ class TestDenoisersOperators:
         for b in range(3):
             assert rel(g[b], R.gaussian_filter(x[b])) <= 1e-13
 
+    def test_convolve_circular_and_device_dft(self, rv, R):
+        import torch
+
+        x = np.random.default_rng(8).uniform(0, 255, (40, 36))
+        psf = rv.make_psf("gaussian", 7, 1.6)
+        ref = R.CirculantBlur(R.psf_taps("gaussian", 7, 1.6), (40, 36))
+        assert rel(rv.convolve_circular(x, psf), ref.apply(x)) <= 1e-13
+        t = torch.from_numpy(x).cuda()
+        assert rel(rv.idft2(rv.dft2(t)).cpu().numpy(), x) <= 1e-14
+
     def test_median_batch_with_ties(self, rv):
         from oracle import extras
 
