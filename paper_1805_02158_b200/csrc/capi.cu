@@ -511,6 +511,7 @@ static int put_taps(redve_ctx* ctx, const double* taps, int k) {
 int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
                   const double* x, double* out) {
   if (B < 1 || H < 1 || W < 1) return fail(ctx, REDVE_E_VALUE, "bad batch shape");
+  if (x == out) return fail(ctx, REDVE_E_VALUE, "out must not alias x (stencils read neighbours)");
   const long long N = (long long)H * W;
   switch (dn->kind) {
     case REDVE_DN_IDENTITY:
@@ -632,6 +633,7 @@ int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, i
                          const double* x, double* out) {
   int rc = op_check(ctx, op, H, W);
   if (rc) return rc;
+  if (x == out) return fail(ctx, REDVE_E_VALUE, "out must not alias x");
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
     RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 0, 1.0, ctx->stream));
@@ -648,6 +650,7 @@ int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B,
                            const double* z, double* out) {
   int rc = op_check(ctx, op, H, W);
   if (rc) return rc;
+  if (z == out) return fail(ctx, REDVE_E_VALUE, "out must not alias z");
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
     RUN(ctx, "conv", launch_conv(z, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 1, 1.0, ctx->stream));

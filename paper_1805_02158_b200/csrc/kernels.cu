@@ -702,13 +702,14 @@ static int pair_chunks(int B, long long N) {
 }
 
 template <int MODE>  // 0: 3x3 median, 1: k x k stencil (corr / conv, scaled)
-__global__ void __launch_bounds__(256) k_pairs(const double* x, double* out, int H, int W,
+__global__ void __launch_bounds__(256) k_pairs(const double* __restrict__ x,
+                                               double* __restrict__ out, int H, int W,
                                                const double* taps, int k, int corr,
                                                double scale) {
   const long long N = (long long)H * W;
   const int b = blockIdx.y;
-  const double* xb = x + (long long)b * N;
-  double* ob = out + (long long)b * N;
+  const double* __restrict__ xb = x + (long long)b * N;
+  double* __restrict__ ob = out + (long long)b * N;
   const int W2 = W >> 1;
   const long long P = N >> 1;
   const long long q0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -716,6 +717,9 @@ __global__ void __launch_bounds__(256) k_pairs(const double* x, double* out, int
   const int di = (int)(stride / W2), dj = (int)(stride % W2);
   int i = (int)(q0 / W2), j2 = (int)(q0 % W2);
   DenoiseArgs dn{DN_MEDIAN3, 0, 1, nullptr};
+  // out never aliases x (operator / denoiser API contract), so unrolled
+  // iterations' loads may issue ahead of the previous stores
+#pragma unroll 4
   for (long long q = q0; q < P; q += stride) {
     const int j = 2 * j2;
     double f0, f1;
@@ -800,6 +804,65 @@ __global__ void __launch_bounds__(256) k_stencil8(const double* x, double* out, 
       ++i;
     }
   }
+}
+
+// Standalone 3x3 median, column-walking: each lane owns one image column and
+// walks down MR rows, loading one new (coalesced) value per output and
+// keeping the sorted 3-row column in registers; neighbours' sorted columns
+// come by warp shuffles.  A warp yields 30 outputs (lanes 0 and 31 are the
+// horizontal halo), so every input byte is read ~1.07x and the only traffic
+// is the image in and f out.
+constexpr int MR = 32;
+
+__global__ void __launch_bounds__(128) k_median_cols(const double* __restrict__ x,
+                                                     double* __restrict__ out, int H, int W) {
+  const long long N = (long long)H * W;
+  const int b = blockIdx.z;
+  const double* __restrict__ xb = x + (long long)b * N;
+  double* __restrict__ ob = out + (long long)b * N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c_out0 = (blockIdx.x * 4 + warp) * 30;  // first output column of this warp
+  const int c = wrap_fast(c_out0 - 1 + lane, W);    // this lane's column
+  const bool emits = lane >= 1 && lane <= 30 && c_out0 - 1 + lane < W;
+  const int r0 = blockIdx.y * MR;
+  const int rend = min(r0 + MR, H);
+  double a = __ldg(xb + (long long)wrap_fast(r0 - 1, H) * W + c);
+  double m = __ldg(xb + (long long)r0 * W + c);
+  // batches of 8 rows: the 8 loads issue before the first median of the batch
+  // (the shuffles keep the compiler from hoisting them by itself)
+  for (int ib = r0; ib < rend; ib += 8) {
+    double nx[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      nx[u] = ib + u < rend ? __ldg(xb + (long long)wrap_fast(ib + u + 1, H) * W + c) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (ib + u >= rend) break;
+      const double e = nx[u];
+      double lo = a, mi = m, hi = e;
+      sort2(lo, mi);
+      sort2(mi, hi);
+      sort2(lo, mi);
+      const double llo = __shfl_up_sync(0xffffffffu, lo, 1),
+                   lmi = __shfl_up_sync(0xffffffffu, mi, 1),
+                   lhi = __shfl_up_sync(0xffffffffu, hi, 1);
+      const double rlo = __shfl_down_sync(0xffffffffu, lo, 1),
+                   rmi = __shfl_down_sync(0xffffffffu, mi, 1),
+                   rhi = __shfl_down_sync(0xffffffffu, hi, 1);
+      if (emits)
+        ob[(long long)(ib + u) * W + c] = med3d(dmax(dmax(llo, lo), rlo), med3d(lmi, mi, rmi),
+                                                dmin(dmin(lhi, hi), rhi));
+      a = m;
+      m = e;
+    }
+  }
+}
+
+static bool launch_median_cols(const double* x, double* out, int B, int H, int W, cudaStream_t s) {
+  if (W < 3 || H < 2) return false;
+  dim3 grid((W + 119) / 120, (H + MR - 1) / MR, B);
+  k_median_cols<<<grid, 128, 0, s>>>(x, out, H, W);
+  return true;
 }
 
 template <int K>
@@ -933,6 +996,7 @@ __global__ void k_median3(const double* x, double* out, int B, int H, int W) {
 }
 void launch_median3(const double* x, double* out, int B, int H, int W, cudaStream_t s) {
   long long N = (long long)H * W;
+  if (launch_median_cols(x, out, B, H, W, s)) return;
   if ((W & 1) == 0 && W >= 4) {
     k_pairs<0><<<dim3(pair_chunks(B, N), B), 256, 0, s>>>(x, out, H, W, nullptr, 3, 0, 1.0);
     return;
