@@ -289,6 +289,34 @@ class TestSolves:
             np.testing.assert_allclose(traces[b].costs(), tro.as_arrays()["cost"], rtol=1e-9)
 
 
+    def test_headline_shape_odd_batch_vs_oracle(self, rv, R):
+        """configs[1]'s path at 256^2 (cadence every 5 steps, the cost identity,
+        VE cycles, CUDA graph) on an odd batch, against the oracle."""
+        from oracle import extras
+        from paper_1805_02158_b200.synth import voronoi_scene
+
+        B, n, budget = 3, 256, 35
+        truths = np.stack([voronoi_scene(s + 20, n) for s in range(B)])
+        op_o = R.CirculantBlur(R.psf_taps("uniform", 9), (n, n))
+        ys = np.stack([R.measure(truths[b], op_o, SQRT2, b) for b in range(B)])
+        op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
+        batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.Median3(), truths)
+        cfg = rv.SolveConfig(method="fp-ve", ve_method="mpe", max_inner_steps=budget)
+        X, traces = rv.solve_batch(batch, ys, cfg)
+        X = X.cpu().numpy()
+        for b in range(B):
+            step, cost = R.red_problem(R.Red(op_o, ys[b], SQRT2, 0.02, extras.median3))
+            xo, tro = R.run_cycling(step, ys[b], budget, "mpe", objective=cost,
+                                    reference=truths[b].ravel())
+            a = tro.as_arrays()
+            assert traces[b].inner_steps == len(tro.iters)
+            assert rel(X[b].ravel(), xo) <= 1e-5
+            np.testing.assert_allclose(traces[b].costs(), a["cost"], rtol=1e-9)
+            np.testing.assert_allclose(traces[b].step_norms(), a["step_norm"], rtol=1e-6)
+            ps = np.array([np.nan if r.psnr is None else r.psnr for r in traces[b].records])
+            np.testing.assert_allclose(ps, a["psnr"], atol=0.01)
+
+
 # --------------------------------------------------------------------- super-resolution
 class TestSuperres:
     def test_patch_weighted_golden(self, rv, golden):
