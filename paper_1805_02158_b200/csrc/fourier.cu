@@ -232,7 +232,7 @@ void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s) {
 
 // --------------------------------------------------------------- columns
 template <int LH>
-__global__ void __launch_bounds__(128, 4) k_col(ColArgs a) {
+__global__ void __launch_bounds__(128, 3) k_col(ColArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
   const bool a0 = takes_step(a.st[b0], a.phase);
   const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
