@@ -149,3 +149,14 @@ def test_two_ranks_match_oracle(method, den, ve_method):
     for k in range(5):
         np.testing.assert_array_equal(out[0][k], out[1][k])
     _compare(out[0], H, W, den, method, budget, ve_method)
+
+
+def test_three_ranks_ragged_slabs_match_oracle():
+    """Three slabs of unequal height (18, 18, 14 rows), the last not ending on
+    a measurement row, the periodic ring closing over three neighbours."""
+    H, W, budget = 50, 47, 14
+    out = _run_world(3, (H, W, "median", "fp-ve", budget, "rre"))
+    for r in (1, 2):
+        for k in range(5):
+            np.testing.assert_array_equal(out[0][k], out[r][k])
+    _compare(out[0], H, W, "median", "fp-ve", budget, "rre")
