@@ -1265,8 +1265,6 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         if (n == clen) {
           RUN(ctx, "gram", launch_gram(va, s));
           CKL();
-          RUN(ctx, "mgs", launch_mgs(va, s));
-          CKL();
           RUN(ctx, "combine", launch_combine(va, s));
           CKL();
           f_ready = false;  // the iterate may have been replaced
@@ -1402,8 +1400,6 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
   va.counters = ctx->ve_counters.as<unsigned>(); va.qscratch = ctx->ve_q.as<double>();
   va.method = method; va.rank_tol = rank_tol; va.chunks = chunks;
   RUN(ctx, "gram", launch_gram(va, s));
-  CKL();
-  RUN(ctx, "mgs", launch_mgs(va, s));
   CKL();
   std::vector<ImgState> pre(B);
   CK(cudaMemcpyAsync(pre.data(), st, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));

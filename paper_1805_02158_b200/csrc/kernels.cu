@@ -354,6 +354,8 @@ __device__ __forceinline__ const double* slot_ptr(const VeArgs& a, int b, int sl
   return a.ring + (long long)b * a.img_stride + (long long)(slot % a.S) * a.slot_stride;
 }
 
+__device__ void mgs_block(const VeArgs& a, int b);
+
 template <int KP1>
 __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
   constexpr int NG = KP1 * (KP1 + 1) / 2;
@@ -445,6 +447,10 @@ __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
       }
     }
   }
+  if (lastb) {  // rank question below the Gram route's resolution: exact MGS, this block
+    __syncthreads();
+    if (s.ve_mode == VE_MGS) mgs_block(a, b);
+  }
 }
 
 template <int KP1>
@@ -480,10 +486,10 @@ __device__ double block_dot(const double* u, const double* v, long long N, doubl
   return s_bc;
 }
 
-__global__ void __launch_bounds__(512) k_mgs(VeArgs a) {
-  const int b = blockIdx.x;
+// The exact MGS route for image b by the whole calling block (any size):
+// called by k_gram's last block for the windows its Gram route flagged.
+__device__ void mgs_block(const VeArgs& a, int b) {
   ImgState& s = a.st[b];
-  if (!ve_participates(s) || s.ve_mode != VE_MGS) return;
   __shared__ double s_red[32];
   __shared__ double R[MAXKP1][MAXKP1];
   __shared__ int s_stop;
@@ -551,7 +557,6 @@ __global__ void __launch_bounds__(512) k_mgs(VeArgs a) {
     }
   }
 }
-void launch_mgs(const VeArgs& a, cudaStream_t s) { k_mgs<<<a.B, 512, 0, s>>>(a); }
 
 // --------------------------------------------------------------- VE: combine
 // x = x_m + sum_{j<k} xi_j (x_{m+j+1} - x_{m+j})  written over the cycle-start

@@ -185,7 +185,6 @@ void launch_cost_fp(const CostArgs& a, int npairs, cudaStream_t s);
 void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
                       cudaStream_t s);
 void launch_gram(const VeArgs& a, cudaStream_t s);
-void launch_mgs(const VeArgs& a, cudaStream_t s);
 void launch_combine(const VeArgs& a, cudaStream_t s);
 void launch_init_state(ImgState* st, int B, cudaStream_t s);
 void launch_gather(double* out, View cur, const double* best, int B, long long N,
