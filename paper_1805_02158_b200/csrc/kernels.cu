@@ -354,7 +354,7 @@ __device__ __forceinline__ const double* slot_ptr(const VeArgs& a, int b, int sl
   return a.ring + (long long)b * a.img_stride + (long long)(slot % a.S) * a.slot_stride;
 }
 
-__device__ void mgs_block(const VeArgs& a, int b);
+__device__ __noinline__ void mgs_block(const VeArgs& a, int b);
 
 template <int KP1>
 __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
@@ -488,7 +488,7 @@ __device__ double block_dot(const double* u, const double* v, long long N, doubl
 
 // The exact MGS route for image b by the whole calling block (any size):
 // called by k_gram's last block for the windows its Gram route flagged.
-__device__ void mgs_block(const VeArgs& a, int b) {
+__device__ __noinline__ void mgs_block(const VeArgs& a, int b) {
   ImgState& s = a.st[b];
   __shared__ double s_red[32];
   __shared__ double R[MAXKP1][MAXKP1];
