@@ -289,6 +289,37 @@ class TestSolves:
             np.testing.assert_allclose(traces[b].costs(), tro.as_arrays()["cost"], rtol=1e-9)
 
 
+    @pytest.mark.parametrize("method", ["fp", "fp-ve"])
+    def test_tolerance_termination_vs_oracle(self, rv, R, method):
+        """tol > 0: per-image convergence stops (non-graph schedule, host
+        checks) at the oracle's step, batch members stopping at different
+        steps."""
+        from oracle import extras
+        from paper_1805_02158_b200.synth import voronoi_scene
+
+        B, n, budget, tol = 3, 64, 120, 2e-3
+        truths = np.stack([voronoi_scene(s + 40, n) for s in range(B)])
+        op_o = R.CirculantBlur(R.psf_taps("uniform", 9), (n, n))
+        ys = np.stack([R.measure(truths[b], op_o, SQRT2 * (1 + b), b) for b in range(B)])
+        op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
+        batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.Median3(), truths)
+        cfg = rv.SolveConfig(method=method, ve_method="rre", max_inner_steps=budget, tol=tol)
+        X, traces = rv.solve_batch(batch, ys, cfg)
+        X = X.cpu().numpy()
+        steps = []
+        for b in range(B):
+            step, cost = R.red_problem(R.Red(op_o, ys[b], SQRT2, 0.02, extras.median3))
+            if method == "fp":
+                xo, tro = R.run_fp(step, ys[b], budget, tol=tol, objective=cost,
+                                   reference=truths[b].ravel())
+            else:
+                xo, tro = R.run_cycling(step, ys[b], budget, "rre", tol=tol, objective=cost,
+                                        reference=truths[b].ravel())
+            assert traces[b].inner_steps == len(tro.iters)
+            assert rel(X[b].ravel(), xo) <= 1e-5
+            steps.append(len(tro.iters))
+        assert max(steps) < budget
+
     def test_headline_shape_odd_batch_vs_oracle(self, rv, R):
         """configs[1]'s path at 256^2 (cadence every 5 steps, the cost identity,
         VE cycles, CUDA graph) on an odd batch, against the oracle."""
