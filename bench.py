@@ -50,15 +50,19 @@ CONFIGS = {
             workload="configs[1]: 64 x 256^2 Voronoi scenes, 9x9 uniform blur, sigma=sqrt(2), "
                      "3x3 median denoiser, FP+MPE m=0 kappa=5, 200 iterations, fp64"),
     2: dict(size=768, batch=1, kind="sr", den="patch", sigma=5.0, ve="rre", scaling="weak",
+            pw_weights="float32",
             workload="configs[2]: one 768^2 Voronoi scene, 7x7 Gaussian blur std 1.6, x3 decimation, "
-                     "sigma=5, PatchWeighted, FP+RRE m=0 kappa=5 with CG, 200 iterations, fp64"),
+                     "sigma=5, PatchWeighted (fp32 weight planes, fp64 arithmetic), FP+RRE m=0 "
+                     "kappa=5 with CG, 200 iterations, fp64"),
     3: dict(size=512, batch=512, kind="deblur", den="filterbank", sigma=SQ2, ve="mpe",
             scaling="strong",
             workload="configs[3]: 512 x 512^2 Voronoi scenes split across the GPUs, 9x9 uniform "
                      "blur, sigma=sqrt(2), seeded 8x5x5 filter bank, FP+MPE, 200 iterations, fp64"),
     4: dict(size=8192, batch=1, kind="sr", den="patch", sigma=5.0, ve="rre", scaling="strong",
+            pw_weights="float32",
             workload="configs[4]: one 8192^2 Voronoi scene (LR 2731^2), 7x7 Gaussian blur std 1.6, "
-                     "x3 decimation, sigma=5, PatchWeighted, FP+RRE m=0 kappa=5 with CG, fp64; "
+                     "x3 decimation, sigma=5, PatchWeighted (fp32 weight planes, fp64 arithmetic), "
+                     "FP+RRE m=0 kappa=5 with CG, fp64; "
                      "row slabs across the GPUs with halo exchange + allreduced inner products; "
                      "one step = the first 7 fixed-point iterations + 1 extrapolation"),
 }
@@ -105,7 +109,9 @@ def product_operator(c):
 def product_denoiser(c):
     import paper_1805_02158_b200 as rv
 
-    return {"gaussian": rv.GaussianFilter, "median": rv.Median3, "patch": rv.PatchWeighted,
+    if c["den"] == "patch":  # BASELINE.json configs[2]/[4]: fp32 storage, fp64 accumulation
+        return rv.PatchWeighted(weight_dtype=c.get("pw_weights", "float64"))
+    return {"gaussian": rv.GaussianFilter, "median": rv.Median3,
             "filterbank": lambda: rv.FilterBank(0)}[c["den"]]()
 
 
@@ -295,8 +301,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
-    """Bytes each kernel must move per launch (each logical array read/written once)."""
+def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20, ws=8):
+    """Bytes each kernel must move per launch (each logical array read/written once);
+    ws = bytes per PatchWeighted raw weight (4 with fp32 planes)."""
     table = {
         "row_fwd": 2 * B * N * s,            # read x, write the pair spectrum
         "col": 2 * B * N * s + N * 8,        # read+write the spectrum, read g
@@ -311,7 +318,7 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
         "cg_update": 6 * B * N * s,          # read x, p, r, q; write x, r
         # raw weights: read x, write the 24 half-plane planes; each balancing sweep:
         # read the planes + D, write D; apply: read planes, D, x, write f
-        "patch_weighted": B * N * s * (1 + npos + iters * (npos + 2) + npos + 3),
+        "patch_weighted": B * N * (s + npos * ws + iters * (npos * ws + 2 * s) + npos * ws + 3 * s),
         # slab primitives of the spatial solve (configs[4])
         "normal_matvec": 2 * B * N * s,      # read w, write out
         "vec_reduce": 2 * B * N * s,         # read x, y
@@ -321,6 +328,10 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20):
         "window_combine": (kp1 + 1) * B * N * s,
     }
     return table.get(kind)
+
+
+def _pw_ws(c):
+    return 4 if c.get("pw_weights") == "float32" else 8
 
 
 def algorithmic_flops(kind, B, N, nf=8, fs=5):
@@ -430,7 +441,7 @@ def run_native(a):
     nat.profile(False)
     kernels = {}
     for kind, (tot, cnt) in rep.items():
-        ab = algorithmic_bytes(kind, B, N)
+        ab = algorithmic_bytes(kind, B, N, ws=_pw_ws(c))
         avg = tot / cnt
         kernels[kind] = {"launches": cnt, "avg_us": 1e3 * avg, "total_ms": tot,
                          "gbs": None if ab is None else ab / (avg / 1e3) / 1e9}
@@ -452,7 +463,7 @@ def run_native(a):
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": None if ach is None else ach / peak, "peak_source": peak_src,
                 "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
-                "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N),
+                "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N, ws=_pw_ws(c)),
                 "traffic": ncu_traffic(dom) if a.config == 1 else None}
 
     # whole-step roofline against SURVEY.md 8(d)'s per-iteration algorithmic
@@ -510,6 +521,7 @@ def run_native(a):
             "config": {"workload": c["workload"], "global_batch": global_batch,
                        "images_per_gpu": B, "image": f"{n}x{n}", "iterations": iters,
                        "ms_per_iteration": ms / max(iters, 1), "parallelism": f"dp{world}",
+                       **({"pw_weight_planes": c["pw_weights"]} if "pw_weights" in c else {}),
                        "l2": "working set > L2 (ring of kappa+2 iterates per image)"
                        if B * N * 8 * (KAPPA + 2) > 126e6 else "working set fits L2"},
             "e2e": {"value": global_batch / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
@@ -604,7 +616,7 @@ def run_spatial(a):
     kernels = {}
     ext_kinds = ("patch_weighted", "normal_matvec", "upsample_corr")
     for kind, (tot, cnt) in rep.items():
-        ab = algorithmic_bytes(kind, 1, Next if kind in ext_kinds else lay.rows * n)
+        ab = algorithmic_bytes(kind, 1, Next if kind in ext_kinds else lay.rows * n, ws=_pw_ws(c))
         avg = tot / cnt
         kernels[kind] = {"launches": cnt, "avg_us": 1e3 * avg, "total_ms": tot,
                          "gbs": None if ab is None else ab / (avg / 1e3) / 1e9}
@@ -617,7 +629,7 @@ def run_spatial(a):
             "frac": ach / peak, "peak_source": peak_src,
             "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
             "algorithmic_bytes_per_launch": algorithmic_bytes(
-                dom, 1, Next if dom in ext_kinds else lay.rows * n), "traffic": None}
+                dom, 1, Next if dom in ext_kinds else lay.rows * n, ws=_pw_ws(c)), "traffic": None}
 
     # e2e through the public API: problem setup from the host measurements (H2D of
     # the slab's y and x0), the solve, the gathered host image out
@@ -643,6 +655,7 @@ def run_spatial(a):
             "config": {"workload": c["workload"], "image": f"{n}x{n}", "iterations": iters,
                        "ms_per_iteration": ms / iters, "parallelism": f"spatial{world}",
                        "slab_rows": lay.rows, "halo_rows": lay.halo,
+                       "pw_weight_planes": c.get("pw_weights", "float64"),
                        "l2": "working set > L2 (8192^2 fp64 = 512 MiB per image)"},
             "e2e": {"value": iters / e2e_s, "unit": "iterations/s",
                     "h2d_bytes_per_step": (lay.Hext + 2 * lay.rows) * n * 8,

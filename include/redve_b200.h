@@ -85,6 +85,9 @@ typedef struct {
   const double* filters;     /* HOST [n_filters][fsize][fsize] */
   const double* scales;      /* HOST [n_filters] */
   double tau;
+  int weight_bits;           /* PATCH: storage of the raw-weight planes, 64 (0 = default)
+                                or 32 (fp32 planes, fp64 arithmetic -- BASELINE.json
+                                configs[2]/[4] "fp32 with fp64 accumulation") */
 } redve_denoiser_desc;
 
 /* SolveConfig (solvers.py:162-199) */

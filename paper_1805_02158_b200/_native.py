@@ -38,7 +38,7 @@ class DenoiserDesc(C.Structure):
         ("patch_radius", C.c_int), ("search_radius", C.c_int), ("balance_iters", C.c_int),
         ("h", C.c_double),
         ("n_filters", C.c_int), ("fsize", C.c_int), ("filters", _dp), ("scales", _dp),
-        ("tau", C.c_double),
+        ("tau", C.c_double), ("weight_bits", C.c_int),
     ]
 
 

@@ -226,6 +226,7 @@ struct redve_problem {
   int dn_api_kind = 0;  // REDVE_DN_* as requested
   int pw_pr = 1, pw_sr = 3, pw_iters = 20, pw_npos = 24;
   double pw_h = 110.0;
+  int pw_w32 = 0;
   DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
   cudaGraphExec_t gexec = nullptr;  // captured solve (Fourier route)
   std::string gkey;
@@ -349,7 +350,8 @@ static int denoise_to_fbuf(redve_problem* p, View x, int phase, double* out = nu
     a.pr = p->pw_pr; a.sr = p->pw_sr; a.npos = p->pw_npos; a.iters = p->pw_iters;
     a.inv_h2 = 1.0 / (p->pw_h * p->pw_h);
     a.xin = x;
-    a.w0 = p->w0.as<double>(); a.D0 = p->D0.as<double>(); a.D1 = p->D1.as<double>();
+    a.w0 = p->w0.as<double>(); a.w32 = p->pw_w32;
+    a.D0 = p->D0.as<double>(); a.D1 = p->D1.as<double>();
     a.out = fdst;
     a.st = p->state.as<ImgState>(); a.phase = phase;
     int n = 0;
@@ -557,6 +559,8 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       if (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1)
         return fail(ctx, REDVE_E_VALUE,
                     "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+      if (dn->weight_bits != 0 && dn->weight_bits != 32 && dn->weight_bits != 64)
+        return fail(ctx, REDVE_E_VALUE, "weight_bits must be 32 or 64");
       const int npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
       CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
       CK(ctx->scratch_a.ensure(sizeof(double) * N * B * npos));
@@ -567,6 +571,7 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
       a.iters = dn->balance_iters; a.inv_h2 = 1.0 / (dn->h * dn->h);
       a.xin = plain(x, N);
       a.w0 = ctx->scratch_a.as<double>();
+      a.w32 = dn->weight_bits == 32;
       a.D0 = ctx->scratch_b.as<double>();
       a.D1 = ctx->scratch_b.as<double>() + N * B;
       a.out = out;
@@ -590,6 +595,8 @@ int redve_patch_weight_maps(redve_ctx* ctx, const redve_denoiser_desc* dn, int B
   if (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1)
     return fail(ctx, REDVE_E_VALUE,
                 "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+  if (dn->weight_bits != 0 && dn->weight_bits != 32 && dn->weight_bits != 64)
+    return fail(ctx, REDVE_E_VALUE, "weight_bits must be 32 or 64");
   const long long N = (long long)H * W;
   const int npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
   CK(ctx->ve_state.ensure(sizeof(ImgState) * B));
@@ -601,6 +608,7 @@ int redve_patch_weight_maps(redve_ctx* ctx, const redve_denoiser_desc* dn, int B
   a.iters = dn->balance_iters; a.inv_h2 = 1.0 / (dn->h * dn->h);
   a.xin = plain(x, N);
   a.w0 = ctx->scratch_a.as<double>();
+  a.w32 = dn->weight_bits == 32;
   a.D0 = ctx->scratch_b.as<double>();
   a.D1 = ctx->scratch_b.as<double>() + N * B;
   a.out = nullptr;
@@ -690,6 +698,9 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
       (dn->patch_radius < 0 || dn->search_radius < 1 || !(dn->h > 0) || dn->balance_iters < 1))
     return fail(ctx, REDVE_E_VALUE,
                 "need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1");
+  if (dn->kind == REDVE_DN_PATCH && dn->weight_bits != 0 && dn->weight_bits != 32 &&
+      dn->weight_bits != 64)
+    return fail(ctx, REDVE_E_VALUE, "weight_bits must be 32 or 64");
   if (dn->kind == REDVE_DN_FILTERBANK &&
       (dn->n_filters < 1 || !is_odd_pos(dn->fsize) || dn->fsize > 15 || !dn->filters || !dn->scales))
     return fail(ctx, REDVE_E_VALUE, "filter bank needs n_filters >= 1 and an odd size <= 15");
@@ -716,6 +727,7 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     p->pw_sr = dn->search_radius;
     p->pw_iters = dn->balance_iters;
     p->pw_h = dn->h;
+    p->pw_w32 = dn->weight_bits == 32;
     p->pw_npos = ((2 * dn->search_radius + 1) * (2 * dn->search_radius + 1) - 1) / 2;
   }
   p->dn_ksize = dn->kind == REDVE_DN_CONV ? dn->ksize : 0;

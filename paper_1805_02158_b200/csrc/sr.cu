@@ -137,7 +137,9 @@ __global__ void k_pw_maps(PwArgs a, const double* D, double* maps) {
   const int H = a.H, W = a.W, sr = a.sr, side = 2 * sr + 1;
   const long long N = (long long)H * W;
   const double* Db = D + (long long)b * N;
-  const double* w0b = a.w0 + (long long)b * a.npos * N;
+  const double* w0b = a.w32 ? reinterpret_cast<const double*>(
+                                  reinterpret_cast<const float*>(a.w0) + (long long)b * a.npos * N)
+                            : a.w0 + (long long)b * a.npos * N;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
@@ -145,14 +147,15 @@ __global__ void k_pw_maps(PwArgs a, const double* D, double* maps) {
       const int di = lin / side - sr, dj = lin % side - sr;
       const int center = (side * side - 1) / 2;
       double w;
-      if (lin == center) {
-        w = 1.0;
-      } else if (lin > center) {
-        w = w0b[(long long)(lin - center - 1) * N + idx];
-      } else {  // negative offset: mirror plane, evaluated at p + o
+      long long wi = -1;
+      if (lin > center) {
+        wi = (long long)(lin - center - 1) * N + idx;
+      } else if (lin < center) {  // negative offset: mirror plane, evaluated at p + o
         const int k = (side * side - 1 - lin) - center - 1;
-        w = w0b[(long long)k * N + (long long)wrap(i + di, H) * W + wrap(j + dj, W)];
+        wi = (long long)k * N + (long long)wrap(i + di, H) * W + wrap(j + dj, W);
       }
+      if (wi < 0) w = 1.0;
+      else w = a.w32 ? (double)reinterpret_cast<const float*>(w0b)[wi] : w0b[wi];
       const double dq = Db[(long long)wrap(i + di, H) * W + wrap(j + dj, W)];
       maps[((long long)b * side * side + lin) * N + idx] = w * Db[idx] * dq;
     }
@@ -177,7 +180,7 @@ constexpr int PW_ROWS = 4;  // output rows per thread (a column strip), 256 thre
 // keeps the (4+2PR) x (2PR+1) patch of x around it in registers; for each
 // offset it forms the squared differences, the separable box sums and the
 // exponential without any block synchronisation.
-template <int PR, int SR>
+template <int PR, int SR, typename WT>
 __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
   constexpr int HALO = PR + SR, X = PW_T + 2 * HALO, P = 2 * PR + 1, R = PW_ROWS + 2 * PR;
   constexpr int NP = HalfPlane<SR>::NPOS;
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
     for (int v = 0; v < P; ++v) xc[u][v] = xs[(ti0 + u) * X + tj0 + v];
   const long long N = (long long)H * W;
   const double inv_box = 1.0 / (P * P);
-  double* w0 = a.w0 + (long long)b * NP * N + (long long)(i0 + oi0) * W + gj;
+  WT* w0 = reinterpret_cast<WT*>(a.w0) + (long long)b * NP * N + (long long)(i0 + oi0) * W + gj;
   const int rows = min(PW_ROWS, H - (i0 + oi0));
 #pragma unroll 2
   for (int k = 0; k < NP; ++k) {
@@ -226,14 +229,15 @@ __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < P; ++t) s += rs[m + t];
-      if (m < rows) w0[(long long)k * N + (long long)m * W] = exp(-fmax(s * inv_box, 0.0) * a.inv_h2);
+      if (m < rows)
+        w0[(long long)k * N + (long long)m * W] = (WT)exp(-fmax(s * inv_box, 0.0) * a.inv_h2);
     }
   }
 }
 
 // Balancing sweep / application with compile-time offsets:
 //   S(p) = v(p) + sum_k [ w0_k(p) v(p+o_k) + w0_k(p-o_k) v(p-o_k) ]
-template <int SR, int RPT>
+template <int SR, int RPT, typename WT>
 __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din, double* Dout,
                                                     int first, int apply) {
   // tile: 32 columns x TH = 8*RPT rows (RPT rows per thread; fewer for small
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
   }
   __syncthreads();
   const bool interior = i0 >= SR && j0 >= SR && i0 + TH + SR <= H && j0 + PW_T + SR <= W;
-  const double* w0b = a.w0 + (long long)b * NP * N;
+  const WT* w0b = reinterpret_cast<const WT*>(a.w0) + (long long)b * NP * N;
   const int oj = threadIdx.x & (PW_T - 1);
   const int gj = j0 + oj;
   if (gj >= W) return;
@@ -278,13 +282,13 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
-      const double* wk = w0b + (long long)k * N;
+      const WT* wk = w0b + (long long)k * N;
       const int sh = di * W + dj;
       double wp[RPT], wm[RPT];
 #pragma unroll
       for (int m = 0; m < RPT; ++m) {
-        wp[m] = __ldg(wk + o[m]);
-        wm[m] = __ldg(wk + o[m] - sh);
+        wp[m] = (double)__ldg(wk + o[m]);
+        wm[m] = (double)__ldg(wk + o[m] - sh);
       }
 #pragma unroll
       for (int m = 0; m < RPT; ++m) {
@@ -296,12 +300,12 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
 #pragma unroll 1
     for (int k = 0; k < NP; ++k) {
       const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
-      const double* wk = w0b + (long long)k * N;
+      const WT* wk = w0b + (long long)k * N;
       const int cm = wrap_fast(gj - dj, W);
 #pragma unroll
       for (int m = 0; m < RPT; ++m) {
-        const double wp = __ldg(wk + o[m]);
-        const double wm = __ldg(wk + (long long)wrap_fast(gi[m] - di, H) * W + cm);
+        const double wp = (double)__ldg(wk + o[m]);
+        const double wm = (double)__ldg(wk + (long long)wrap_fast(gi[m] - di, H) * W + cm);
         S[m] = fma(wp, vs[(ci[m] + di) * X + cj + dj], S[m]);
         S[m] = fma(wm, vs[(ci[m] - di) * X + cj - dj], S[m]);
       }
@@ -316,44 +320,169 @@ __global__ void __launch_bounds__(256) k_pw_sweep_t(PwArgs a, const double* Din,
   }
 }
 
-template <int SR, int RPT>
+// Vectorised sweep: each thread owns VW = 16 / sizeof(WT) adjacent outputs of
+// one row, so every plane read is a 16-byte load (4 fp32 or 2 fp64 weights).
+// The sweep is bound by outstanding load requests, not bytes (ncu: long-
+// scoreboard stalls at 3.1 TB/s for both plane widths with one output per
+// thread), so fewer, wider requests are what moves it toward the HBM roof.
+// The mirrored weight w0_k(p - o_k) starts -dj columns off the vector grid:
+// for dj % VW != 0 it is spliced from two aligned loads (compile-time lanes).
+template <int VW>
+struct VecSplit {  // q = -dj split as VW * qb + qr, 0 <= qr < VW
+  __host__ __device__ static constexpr int qb(int q) { return q >= 0 ? q / VW : -((-q + VW - 1) / VW); }
+  __host__ __device__ static constexpr int qr(int q) { return q - VW * qb(q); }
+};
+
+template <typename WT>
+union WVec {
+  int4 raw;
+  WT e[16 / sizeof(WT)];
+};
+
+template <int SR, typename WT>
+__global__ void __launch_bounds__(256) k_pw_sweep_v(PwArgs a, const double* Din, double* Dout,
+                                                    int first, int apply) {
+  constexpr int VW = 16 / sizeof(WT), TW = 32 * VW, TH = 8;
+  constexpr int X = TW + 2 * SR, Y = TH + 2 * SR, NP = HalfPlane<SR>::NPOS;
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W;
+  double* vs = reinterpret_cast<double*>(s_smem);
+  const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+  const long long N = (long long)H * W;
+  const double* Db = Din + (long long)b * N;
+  const double* x = apply ? a.xin.at(b, a.st) : nullptr;
+  for (int idx = threadIdx.x; idx < Y * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    const long long o = (long long)wrap_fast(i0 - SR + ti, H) * W + wrap_fast(j0 - SR + tj, W);
+    const double d = first ? 1.0 : __ldg(Db + o);
+    vs[idx] = apply ? d * __ldg(x + o) : d;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, oi = threadIdx.x >> 5;
+  const int gj = j0 + VW * lane;
+  if (gj >= W) return;
+  const int gi = min(i0 + oi, H - 1);  // rows past the image edge compute a throwaway copy
+  const int ci = gi - i0 + SR, cj = VW * lane + SR;
+  const long long o = (long long)gi * W + gj;
+  const WT* w0b = reinterpret_cast<const WT*>(a.w0) + (long long)b * NP * N;
+  double S[VW];
+#pragma unroll
+  for (int t = 0; t < VW; ++t) S[t] = vs[ci * X + cj + t];
+  const bool interior = i0 >= SR && i0 + TH + SR <= H && j0 >= 2 * VW && j0 + TW + 2 * VW <= W;
+  if (interior) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+      const WT* wk = w0b + (long long)k * N;
+      WVec<WT> wp, lo, hi;
+      wp.raw = __ldg(reinterpret_cast<const int4*>(wk + o));
+      const long long om = o - (long long)di * W + VW * VecSplit<VW>::qb(-dj);
+      lo.raw = __ldg(reinterpret_cast<const int4*>(wk + om));
+      if (VecSplit<VW>::qr(-dj) != 0) hi.raw = __ldg(reinterpret_cast<const int4*>(wk + om + VW));
+      else hi.raw = lo.raw;
+#pragma unroll
+      for (int t = 0; t < VW; ++t) {
+        const int u = t + VecSplit<VW>::qr(-dj);
+        const double wm = (double)(u < VW ? lo.e[u < VW ? u : 0] : hi.e[u >= VW ? u - VW : 0]);
+        S[t] = fma((double)wp.e[t], vs[(ci + di) * X + cj + t + dj], S[t]);
+        S[t] = fma(wm, vs[(ci - di) * X + cj + t - dj], S[t]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < NP; ++k) {
+      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+      const WT* wk = w0b + (long long)k * N;
+      const long long rm = (long long)wrap_fast(gi - di, H) * W;
+#pragma unroll
+      for (int t = 0; t < VW; ++t) {
+        const double wp = (double)__ldg(wk + o + t);
+        const double wm = (double)__ldg(wk + rm + wrap_fast(gj + t - dj, W));
+        S[t] = fma(wp, vs[(ci + di) * X + cj + t + dj], S[t]);
+        S[t] = fma(wm, vs[(ci - di) * X + cj + t - dj], S[t]);
+      }
+    }
+  }
+  if (i0 + oi >= H) return;
+#pragma unroll
+  for (int t = 0; t < VW; ++t) {
+    const double d = first ? 1.0 : Db[o + t];
+    if (apply) a.out[(long long)b * N + o + t] = d * S[t];
+    else Dout[(long long)b * N + o + t] = d / sqrt(d * S[t]);
+  }
+}
+
+template <int SR, typename WT>
+static void pw_sweeps_v(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
+  constexpr int VW = 16 / sizeof(WT), TW = 32 * VW;
+  dim3 grid(cdivs(a.W, TW), cdivs(a.H, 8), a.B);
+  const size_t sm = sizeof(double) * (TW + 2 * SR) * (8 + 2 * SR);
+  const double* din = a.D0;
+  double* dout = a.D1;
+  for (int it = 0; it < a.iters; ++it) {
+    k_pw_sweep_v<SR, WT><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    ++*launches;
+    din = dout;
+    dout = (dout == a.D1) ? a.D0 : a.D1;
+  }
+  if (with_apply) {
+    k_pw_sweep_v<SR, WT><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+    ++*launches;
+  }
+}
+
+template <int SR, int RPT, typename WT>
 static void pw_sweeps_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
   dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, 8 * RPT), a.B);
   const size_t sm = sizeof(double) * (PW_T + 2 * SR) * (8 * RPT + 2 * SR);
   const double* din = a.D0;
   double* dout = a.D1;
   for (int it = 0; it < a.iters; ++it) {
-    k_pw_sweep_t<SR, RPT><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    k_pw_sweep_t<SR, RPT, WT><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
     ++*launches;
     din = dout;
     dout = (dout == a.D1) ? a.D0 : a.D1;
   }
   if (with_apply) {
-    k_pw_sweep_t<SR, RPT><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+    k_pw_sweep_t<SR, RPT, WT><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
     ++*launches;
   }
 }
 
-template <int PR, int SR>
+template <int PR, int SR, typename WT>
 static void pw_pass_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
   dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
   constexpr int X = PW_T + 2 * (PR + SR);
-  k_pw_weights_t<PR, SR><<<grid, 256, sizeof(double) * X * X, s>>>(a);
+  k_pw_weights_t<PR, SR, WT><<<grid, 256, sizeof(double) * X * X, s>>>(a);
   ++*launches;
   // rows per thread: 1 measured best at every size (768^2: 0.91 ms vs 1.30 ms
   // with 4; 4096^2: 14.7 vs 21.8 ms) -- more, smaller CTAs hide the latency
   int rpt = 1;
   if (const char* e = getenv("REDVE_PW_RPT")) rpt = atoi(e);  // experiments
-  if (rpt == 4) pw_sweeps_t<SR, 4>(a, s, launches, with_apply);
-  else if (rpt == 2) pw_sweeps_t<SR, 2>(a, s, launches, with_apply);
-  else pw_sweeps_t<SR, 1>(a, s, launches, with_apply);
+  // the vector sweep pays on large images (4096^2 fp32: 13.8 -> 12.9 ms per
+  // call); below ~8 waves of its 4x larger CTAs the scalar sweep is faster
+  // (768^2 fp32: 0.69 vs 0.89 ms)
+  constexpr int VW = 16 / (int)sizeof(WT);
+  const long long vec_ctas = (long long)cdivs(a.W, 32 * VW) * cdivs(a.H, 8) * a.B;
+  bool vec = a.W % VW == 0 && a.W >= 32 * VW && vec_ctas >= 8LL * 148 * 4;
+  if (const char* e = getenv("REDVE_PW_VEC")) vec = e[0] == '1' ? (a.W % VW == 0 && a.W >= 32 * VW)
+                                                                : false;
+  if (vec) {
+    pw_sweeps_v<SR, WT>(a, s, launches, with_apply);
+    return;
+  }
+  if (rpt == 4) pw_sweeps_t<SR, 4, WT>(a, s, launches, with_apply);
+  else if (rpt == 2) pw_sweeps_t<SR, 2, WT>(a, s, launches, with_apply);
+  else pw_sweeps_t<SR, 1, WT>(a, s, launches, with_apply);
 }
 
 // true if a specialisation ran; the final D is in D0 if iters is even, else D1
 static bool pw_specialised(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
 #define PW_CASE(PRV, SRV)                                  \
   if (a.pr == PRV && a.sr == SRV) {                        \
-    pw_pass_t<PRV, SRV>(a, s, launches, with_apply);       \
+    if (a.w32) pw_pass_t<PRV, SRV, float>(a, s, launches, with_apply);  \
+    else pw_pass_t<PRV, SRV, double>(a, s, launches, with_apply);      \
     return true;                                           \
   }
   PW_CASE(1, 3) PW_CASE(1, 1) PW_CASE(1, 2) PW_CASE(0, 3) PW_CASE(2, 3) PW_CASE(0, 1)
@@ -361,12 +490,14 @@ static bool pw_specialised(const PwArgs& a, cudaStream_t s, int* launches, bool 
   return false;
 }
 
-void launch_pw_maps(const PwArgs& a, cudaStream_t s, int* launches, double* maps) {
-  dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
+void launch_pw_maps(const PwArgs& a_in, cudaStream_t s, int* launches, double* maps) {
+  dim3 grid(cdivs(a_in.W, PW_T), cdivs(a_in.H, PW_T), a_in.B);
+  PwArgs a = a_in;
   const double* din = a.D0;
   if (pw_specialised(a, s, launches, false)) {
     din = (a.iters % 2 == 0) ? a.D0 : a.D1;
   } else {
+    a.w32 = 0;  // the generic kernels keep fp64 planes
     k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
     const size_t sm = sizeof(double) * (PW_T + 2 * a.sr) * (PW_T + 2 * a.sr);
     double* dout = a.D1;
@@ -386,8 +517,10 @@ size_t pw_weights_smem(int pr, int sr) {
   return sizeof(double) * ((size_t)X * X + (size_t)E * E + (size_t)E * PW_T);
 }
 
-void launch_pw(const PwArgs& a, cudaStream_t s, int* launches) {
-  if (pw_specialised(a, s, launches, true)) return;
+void launch_pw(const PwArgs& a_in, cudaStream_t s, int* launches) {
+  if (pw_specialised(a_in, s, launches, true)) return;
+  PwArgs a = a_in;
+  a.w32 = 0;  // the generic kernels keep fp64 planes
   dim3 grid(cdivs(a.W, PW_T), cdivs(a.H, PW_T), a.B);
   k_pw_weights<<<grid, 256, pw_weights_smem(a.pr, a.sr), s>>>(a);
   ++*launches;

@@ -12,6 +12,7 @@ struct PwArgs {
   double inv_h2;
   View xin;          // images to denoise
   double* w0;        // [B][npos][N] raw weights of the half-plane offsets
+  int w32;           // 1: w0 holds fp32 planes (specialised radii; arithmetic stays fp64)
   double* D0;        // [B][N] balancing field, ping-pong
   double* D1;
   double* out;       // [B][N] f(x)

@@ -97,20 +97,30 @@ class PatchWeighted(_Native):
     linear = False
 
     def __init__(self, patch_radius: int = 1, search_radius: int = 3, h: float = 110.0,
-                 balance_iters: int = 20):
+                 balance_iters: int = 20, weight_dtype: str = "float64"):
+        """``weight_dtype`` (not in the reference): storage of the raw-weight
+        planes.  "float32" halves the sweeps' HBM traffic (BASELINE.json
+        configs[2]/[4]: "fp32 with fp64 ... accumulation"); every product and
+        sum stays fp64, the weights carry a 2^-24 relative rounding."""
         if patch_radius < 0 or search_radius < 1 or h <= 0 or balance_iters < 1:
             raise ValueError("need patch_radius >= 0, search_radius >= 1, h > 0, balance_iters >= 1")
+        if weight_dtype not in ("float64", "float32"):
+            raise ValueError("weight_dtype must be 'float64' or 'float32'")
         self.patch_radius = int(patch_radius)
         self.search_radius = int(search_radius)
         self.h = float(h)
         self.balance_iters = int(balance_iters)
+        self.weight_dtype = weight_dtype
         self.name = f"patch_weighted(p={patch_radius},s={search_radius},h={h:g})"
+        if weight_dtype == "float32":
+            self.name += "[fp32 weights]"
 
     def _fill(self, d):
         d.patch_radius = self.patch_radius
         d.search_radius = self.search_radius
         d.balance_iters = self.balance_iters
         d.h = self.h
+        d.weight_bits = 32 if self.weight_dtype == "float32" else 64
 
     def weight_maps(self, x):
         """(offsets, maps): the balanced weight of every search offset (denoisers.py:83-111)."""

@@ -359,7 +359,8 @@ class TestSuperres:
                 n += 1
         assert n >= 3
 
-    @pytest.mark.parametrize("shape", [(32, 40), (96, 96), (70, 33), (200, 170), (5, 7)])
+    @pytest.mark.parametrize("shape", [(32, 40), (96, 96), (70, 33), (200, 170), (5, 7),
+                                       (136, 260), (24, 520)])
     def test_patch_weighted_vs_oracle(self, rv, R, shape):
         x = np.random.default_rng(7).uniform(0, 255, shape)
         assert rel(rv.PatchWeighted()(x), R.patch_weighted(x)) <= 1e-12
@@ -415,6 +416,59 @@ class TestSuperres:
             x = rng.uniform(0, 255, shape)
             assert abs(obj.cost(x) - red.cost(x)) <= 1e-10 * abs(red.cost(x))
             assert rel(obj.fp_step(x), red.fp_step(x)) <= 1e-9
+
+
+class TestPatchWeightedFp32Planes:
+    """PatchWeighted(weight_dtype="float32"): raw-weight planes stored in fp32,
+    fp64 arithmetic (BASELINE.json configs[2]/[4] precision).  Tolerances: the
+    denoiser within 1e-6 relative of the fp64 reference (a 2^-24 rounding of
+    each weight), whole solves within north_star's 1e-5 / same iteration
+    count / PSNR 0.01 dB."""
+
+    @pytest.mark.parametrize("shape", [(96, 96), (70, 33), (200, 170), (5, 7), (136, 260),
+                                       (24, 520), (256, 256)])
+    def test_denoiser_vs_oracle(self, rv, R, shape):
+        x = np.random.default_rng(17).uniform(0, 255, shape)
+        got = rv.PatchWeighted(weight_dtype="float32")(x)
+        e = rel(got, R.patch_weighted(x))
+        assert e <= 1e-6
+        assert e > 1e-14  # the fp32 planes are really in use
+        e2 = rel(rv.PatchWeighted(1, 2, 60.0, 7, weight_dtype="float32")(x),
+                 R.patch_weighted(x, 1, 2, 60.0, 7))
+        assert e2 <= 1e-6
+
+    def test_generic_radii_keep_fp64(self, rv, R):
+        # radii without a compile-time specialisation run the generic fp64 kernels
+        x = np.random.default_rng(18).uniform(0, 255, (40, 36))
+        got = rv.PatchWeighted(3, 1, 80.0, 5, weight_dtype="float32")(x)
+        assert rel(got, R.patch_weighted(x, 3, 1, 80.0, 5)) <= 1e-12
+
+    def test_weight_maps(self, rv, R):
+        x = np.random.default_rng(8).uniform(0, 255, (20, 24))
+        offs, maps = rv.PatchWeighted(weight_dtype="float32").weight_maps(x)
+        offs_o, maps_o = R.patch_weight_maps(x)
+        assert offs == offs_o
+        for a, b in zip(maps, maps_o):
+            np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-12)
+
+    @pytest.mark.parametrize("name,method,ve_method", [("fp", "fp", "mpe"), ("rre", "fp-ve", "rre")])
+    def test_sr48_solve_vs_reference(self, rv, golden, name, method, ve_method):
+        g = golden("superres.npz")
+        truth, y, x0 = g["sr48/truth"], g["sr48/y"], g["sr48/x0"]
+        op = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, truth.shape)
+        obj = rv.RedObjective(op, y, 5.0, 0.02, rv.PatchWeighted(weight_dtype="float32"))
+        prob = rv.as_fixed_point_problem(obj, reference=truth)
+        x, tr = rv.solve(prob, x0.ravel(), rv.SolveConfig(method=method, ve_method=ve_method,
+                                                          max_inner_steps=30))
+        assert rel(x, g[f"sr48/{name}/x"]) <= 1e-5
+        ref_psnr = g[f"sr48/{name}/psnr"]
+        ps = np.array([np.nan if r.psnr is None else r.psnr for r in tr.records])
+        assert len(ps) == len(ref_psnr)  # same number of iterations
+        np.testing.assert_allclose(ps, ref_psnr, atol=0.01)
+
+    def test_bad_weight_dtype(self, rv):
+        with pytest.raises(ValueError):
+            rv.PatchWeighted(weight_dtype="float16")
 
 
 # --------------------------------------------------------------------- filter bank (configs[3])

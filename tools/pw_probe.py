@@ -1,6 +1,6 @@
 """Time one PatchWeighted call (and the SR normal operator) at a given size.
 
-python tools/pw_probe.py [n] [reps]"""
+python tools/pw_probe.py [n] [reps] [float64|float32]"""
 import os
 import sys
 
@@ -18,7 +18,8 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     g = np.random.default_rng(0)
     x = torch.from_numpy(g.uniform(0, 255, (n, n))).cuda()
-    den = rv.PatchWeighted()
+    wdt = sys.argv[3] if len(sys.argv) > 3 else "float64"
+    den = rv.PatchWeighted(weight_dtype=wdt)
     den(x)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -29,8 +30,9 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     N = n * n
-    print(f"patch_weighted {n}x{n}: {ms:.3f} ms/call; 24-plane sweep floor "
-          f"{20 * 24 * 8 * N / 6.5e12 * 1e3:.2f} ms")
+    ws = 4 if wdt == "float32" else 8
+    print(f"patch_weighted[{wdt}] {n}x{n}: {ms:.3f} ms/call; 24-plane sweep floor "
+          f"{20 * 24 * ws * N / 6.5e12 * 1e3:.2f} ms")
     fwd = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, (n, n))
     ops = NativeSlabOps(fwd, 5.0, 0.02, den)
     ops.normal_matvec(x, 0, n)
