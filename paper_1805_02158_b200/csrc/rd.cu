@@ -233,6 +233,120 @@ __global__ void __launch_bounds__(256) k_rd_bank8(RdArgs a) {
   }
 }
 
+// Wide-tile variant (the default): 64 x 64 outputs per CTA, every thread a
+// 2-column block (influence: 2 x 10 rows, adjoint: 2 x 8 rows), so each
+// 16-byte shared-memory read feeds two output columns.  ncu on k_rd_bank8:
+// FP64 pipe 67% with shared-memory wavefronts at 70% (LDS.64, 2.4 bytes per
+// FMA) and 52 of 256 threads idle in the influence pass; here 1.4 bytes per
+// FMA and 238 / 256 threads busy in the influence pass.
+constexpr int RW_T = 64, RW_S1 = 10, RW_S2 = 8;
+constexpr int RW_PW = RW_T + 4, RW_PH = 7 * RW_S1;   // influence tile (68 used rows of 70)
+constexpr int RW_X = RW_T + 8, RW_XH = RW_PH + 4;    // x tile: 72 columns x 74 rows
+constexpr size_t rw_smem() { return sizeof(double) * ((size_t)RW_X * RW_XH + (size_t)RW_PH * RW_PW); }
+
+__global__ void __launch_bounds__(256, 2) k_rd_bank8w(RdArgs a) {
+  constexpr int FS = RB_FS, NF = RB_NF;
+  const int b = blockIdx.z;
+  if (!takes_step(a.st[b], a.phase)) return;
+  const int H = a.H, W = a.W;
+  __shared__ double s_isc[NF];
+  if (threadIdx.x < NF) s_isc[threadIdx.x] = 1.0 / (a.scales[threadIdx.x] * a.scales[threadIdx.x]);
+  double* xs = reinterpret_cast<double*>(r_smem);  // rows i0-4 .., columns j0-4 ..
+  double* ph = xs + RW_X * RW_XH;                   // rows i0-2 .., columns j0-2 ..
+  const int i0 = blockIdx.y * RW_T, j0 = blockIdx.x * RW_T;
+  const double* x = a.xin.at(b, a.st);
+  for (int idx = threadIdx.x; idx < RW_X * RW_XH; idx += blockDim.x) {
+    const int ti = idx / RW_X, tj = idx - ti * RW_X;
+    xs[idx] = __ldg(x + (long long)wrap(i0 - 4 + ti, H) * W + wrap(j0 - 4 + tj, W));
+  }
+  const int t = threadIdx.x;
+  const bool p1 = t < (RW_PW / 2) * (RW_PH / RW_S1);
+  const int pc = 2 * (t % (RW_PW / 2)), pr0 = (t / (RW_PW / 2)) * RW_S1;
+  const int oc = 2 * (t & 31), or0 = (t >> 5) * RW_S2;
+  double acc[RW_S2][2];
+#pragma unroll
+  for (int m = 0; m < RW_S2; ++m) acc[m][0] = acc[m][1] = 0.0;
+  __syncthreads();
+#pragma unroll 1
+  for (int f = 0; f < NF; ++f) {
+    const double* kf = c_rb_taps + f * FS * FS;
+    if (p1) {  // phi over influence rows pr0.., columns pc, pc+1: x rows pr0+ta, columns pc+tb
+      double z[RW_S1][2];
+#pragma unroll
+      for (int m = 0; m < RW_S1; ++m) z[m][0] = z[m][1] = 0.0;
+#pragma unroll
+      for (int u = 0; u < RW_S1 + FS - 1; ++u) {
+        double xv[6];
+        const double2* row = reinterpret_cast<const double2*>(xs + (pr0 + u) * RW_X + pc);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double2 v = row[q];
+          xv[2 * q] = v.x;
+          xv[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int m = 0; m < RW_S1; ++m) {
+          const int ta = u - m;
+          if (ta < 0 || ta >= FS) continue;
+#pragma unroll
+          for (int tb = 0; tb < FS; ++tb) {
+            const double kk = kf[ta * FS + tb];
+            z[m][0] = fma(kk, xv[tb], z[m][0]);
+            z[m][1] = fma(kk, xv[tb + 1], z[m][1]);
+          }
+        }
+      }
+      const double isc = s_isc[f];
+#pragma unroll
+      for (int m = 0; m < RW_S1; ++m) {
+        double2 o;
+        o.x = z[m][0] / fma(z[m][0] * z[m][0], isc, 1.0);
+        o.y = z[m][1] / fma(z[m][1] * z[m][1], isc, 1.0);
+        *reinterpret_cast<double2*>(ph + (pr0 + m) * RW_PW + pc) = o;
+      }
+    }
+    __syncthreads();
+    // adjoint: out(r, c) += k[ta][tb] phi(r + 2 - ta, c + 2 - tb); phi rows or0 + m + 4 - ta,
+    // columns oc + 4 - tb (+1 for the second column)
+#pragma unroll
+    for (int u = 0; u < RW_S2 + FS - 1; ++u) {
+      double pv[6];
+      const double2* row = reinterpret_cast<const double2*>(ph + (or0 + u) * RW_PW + oc);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double2 v = row[q];
+        pv[2 * q] = v.x;
+        pv[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int m = 0; m < RW_S2; ++m) {
+        const int ta = m + 4 - u;
+        if (ta < 0 || ta >= FS) continue;
+#pragma unroll
+        for (int tb = 0; tb < FS; ++tb) {
+          const double kk = kf[ta * FS + tb];
+          acc[m][0] = fma(kk, pv[4 - tb], acc[m][0]);
+          acc[m][1] = fma(kk, pv[5 - tb], acc[m][1]);
+        }
+      }
+    }
+    __syncthreads();  // phi is overwritten by the next filter
+  }
+  const long long N = (long long)H * W;
+#pragma unroll
+  for (int m = 0; m < RW_S2; ++m) {
+    const int gi = i0 + or0 + m;
+    if (gi >= H) break;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int gj = j0 + oc + c;
+      if (gj >= W) continue;
+      const double xv = xs[(or0 + m + 4) * RW_X + (oc + c + 4)];
+      a.out[(long long)b * N + (long long)gi * W + gj] = fma(-a.tau, acc[m][c], xv);
+    }
+  }
+}
+
 static bool launch_rd_bank8(const RdArgs& a, cudaStream_t s) {
   if (a.nf != RB_NF || a.fs != RB_FS) return false;
   static bool done = false;
@@ -246,6 +360,17 @@ static bool launch_rd_bank8(const RdArgs& a, cudaStream_t s) {
   constexpr int R = RB_FS / 2;
   const size_t smem = sizeof(double) * ((size_t)(RB_TW + 4 * R) * (RB_TH + 4 * R) +
                                         2 * (size_t)(RB_TW + 2 * R) * (RB_TH + 2 * R));
+  const char* e = getenv("REDVE_FB_WIDE");
+  if (!(e && e[0] == '0')) {
+    static bool wdone = false;
+    if (!wdone) {
+      cudaFuncSetAttribute(k_rd_bank8w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rw_smem());
+      wdone = true;
+    }
+    dim3 gw((a.W + RW_T - 1) / RW_T, (a.H + RW_T - 1) / RW_T, a.B);
+    k_rd_bank8w<<<gw, 256, rw_smem(), s>>>(a);
+    return true;
+  }
   dim3 grid((a.W + RB_TW - 1) / RB_TW, (a.H + RB_TH - 1) / RB_TH, a.B);
   k_rd_bank8<<<grid, 256, smem, s>>>(a);
   return true;

@@ -473,13 +473,21 @@ class TestPatchWeightedFp32Planes:
 
 # --------------------------------------------------------------------- filter bank (configs[3])
 class TestFilterBank:
-    @pytest.mark.parametrize("shape", [(32, 32), (64, 48), (100, 70)])
+    @pytest.mark.parametrize("shape", [(32, 32), (64, 48), (100, 70), (130, 200), (512, 512)])
     def test_vs_oracle(self, rv, shape):
         from oracle import extras
 
         x = np.random.default_rng(11).uniform(0, 255, shape)
         for seed in (0, 3):
             assert rel(rv.FilterBank(seed)(x), extras.FilterBank(seed)(x)) <= 1e-13
+
+    def test_wide_and_narrow_tiles_agree(self, rv, monkeypatch):
+        # the 64x64 wide-tile kernel (default) against the 64x32 one (REDVE_FB_WIDE=0)
+        x = np.random.default_rng(12).uniform(0, 255, (3, 96, 160))
+        wide = rv.FilterBank(1)(x)
+        monkeypatch.setenv("REDVE_FB_WIDE", "0")
+        narrow = rv.FilterBank(1)(x)
+        assert rel(wide, narrow) <= 1e-14
 
     def test_deblur_solve_vs_oracle(self, rv, R):
         from oracle import extras
