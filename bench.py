@@ -632,7 +632,14 @@ def run_spatial(a):
                 dom, 1, Next if dom in ext_kinds else lay.rows * n, ws=_pw_ws(c)), "traffic": None}
 
     # e2e through the public API: problem setup from the host measurements (H2D of
-    # the slab's y and x0), the solve, the gathered host image out
+    # the slab's y and x0), the solve, the gathered host image out.  The timed
+    # problem is released first so the new one reuses its device blocks (a user
+    # runs one problem of this size at a time).
+    del one_step, prob, x0_slab, tr
+    import gc
+
+    gc.collect()
+    torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
     prob2 = SpatialProblem(op, y, c["sigma"], ALPHA, den, comm=comm, reference=truth)

@@ -260,11 +260,13 @@ class SpatialProblem:
         self.lay = SlabLayout(H, W, self.s, self.comm.world, self.comm.rank, halo)
         lay = self.lay
         y = np.asarray(y, dtype=np.float64)
-        yup = np.zeros((lay.Hext, W))
-        for u, g in enumerate(lay.ext_rows()):
-            if g % self.s == 0:
-                yup[u, ::self.s] = y[g // self.s]
-        self.yup = self.ops.tensor(yup)
+        # zero-filled upsampling of the slab's measurement rows, built on the
+        # device: only the LR rows the slab touches cross the bus
+        rows = [(u, g // self.s) for u, g in enumerate(lay.ext_rows()) if g % self.s == 0]
+        yup = self.ops.zeros((lay.Hext, W))
+        if rows:
+            yup[[u for u, _ in rows], ::self.s] = self.ops.tensor(y[[g for _, g in rows]])
+        self.yup = yup
         self.hty = self.ops.correlate(self.yup, 1.0 / self.sigma**2)[lay.halo: lay.halo + lay.rows]
         self.ref = None if reference is None else self.ops.tensor(
             np.asarray(reference, dtype=np.float64)[lay.start: lay.stop])
