@@ -665,7 +665,8 @@ def run_spatial(a):
                        "pw_weight_planes": c.get("pw_weights", "float64"),
                        "l2": "working set > L2 (8192^2 fp64 = 512 MiB per image)"},
             "e2e": {"value": iters / e2e_s, "unit": "iterations/s",
-                    "h2d_bytes_per_step": (lay.Hext + 2 * lay.rows) * n * 8,
+                    "h2d_bytes_per_step": (sum(1 for g in lay.ext_rows() if g % 3 == 0)
+                                           * ((n + 2) // 3) + 2 * lay.rows * n) * 8,
                     "d2h_bytes_per_step": n * n * 8, "ms_per_step": 1e3 * e2e_s},
             "gpu_launches": int((l1 - l0) // a.steps),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "clocks": clk,
