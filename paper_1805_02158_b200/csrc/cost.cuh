@@ -55,7 +55,10 @@ __device__ __forceinline__ void conv_span(cd (&f)[16], const cd* tile, const Til
   constexpr int r = K / 2;
 #pragma unroll
   for (int j = 0; j < 16; ++j) f[j] = cd{0.0, 0.0};
-#pragma unroll
+  // the tap rows stay a loop: fully unrolled, the 5x5 body is ~800 FMAs of
+  // straight-line code per span and a single-image solve (configs[0], few
+  // warps per SM) stalls on instruction fetch (ncu: no_instruction)
+#pragma unroll 1
   for (int ta = 0; ta < K; ++ta) {
     cd row[16 + K - 1];  // columns c0 - r .. c0 + 15 + r of tile row ti - (ta - r)
 #pragma unroll
@@ -118,6 +121,34 @@ __device__ __forceinline__ void denoise_span(cd (&f)[16], const cd* tile, const 
   }
 }
 
+// K x K correlation at the pixel pair (i, j), (i, j+1), K known at compile
+// time: the K+1 wrapped columns are formed once and every row's K+1 values
+// feed both outputs (same terms and order as fk_pair's runtime loop).
+template <int K>
+__device__ __forceinline__ void conv_pair(const double* x, int H, int W, int i, int j,
+                                          const double* taps, double& f0, double& f1) {
+  constexpr int r = K / 2;
+  int cols[K + 1];  // columns j - r .. j + 1 + r
+#pragma unroll
+  for (int u = 0; u <= K; ++u) cols[u] = wrap_fast(j - r + u, W);
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int ta = 0; ta < K; ++ta) {
+    const double* row = x + (long long)wrap_fast(i - (ta - r), H) * W;
+    double v[K + 1];
+#pragma unroll
+    for (int u = 0; u <= K; ++u) v[u] = __ldg(row + cols[u]);
+#pragma unroll
+    for (int tb = 0; tb < K; ++tb) {
+      const double w = taps[ta * K + tb];
+      a0 = fma(w, v[2 * r - tb], a0);
+      a1 = fma(w, v[2 * r - tb + 1], a1);
+    }
+  }
+  f0 = a0;
+  f1 = a1;
+}
+
 // f(x) at the pixel pair (i, j), (i, j+1) of one image from L1-resident
 // neighbours (periodic): the streaming kernels' denoiser (cost.cu k_cost_fp,
 // kernels.cu k_median3_pairs).
@@ -147,6 +178,9 @@ __device__ __forceinline__ void fk_pair(const double* x, int H, int W, int i, in
                dmin(dmin(c[0][2], c[1][2]), c[2][2]));
     f1 = med3d(dmax(dmax(c[1][0], c[2][0]), c[3][0]), med3d(c[1][1], c[2][1], c[3][1]),
                dmin(dmin(c[1][2], c[2][2]), c[3][2]));
+  } else if (DK == DN_CONV && (dn.ksize == 3 || dn.ksize == 5)) {
+    if (dn.ksize == 5) conv_pair<5>(x, H, W, i, j, taps, f0, f1);
+    else conv_pair<3>(x, H, W, i, j, taps, f0, f1);
   } else if (DK == DN_CONV) {
     const int k = dn.ksize, r = k >> 1;
     double a0 = 0.0, a1 = 0.0;
