@@ -1,0 +1,52 @@
+"""bench.py's bookkeeping (CPU): the algorithmic byte / flop models DESIGN.md
+section 3 states, the config table against BASELINE.json, the unit scaling."""
+
+import importlib.util
+import json
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_configs_cover_baseline(bench):
+    base = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+    assert sorted(bench.CONFIGS) == list(range(len(base["configs"])))
+    for i, c in bench.CONFIGS.items():
+        assert c["workload"].startswith(f"configs[{i}]")
+    # the super-resolution configs use BASELINE's fp32 storage, everything else fp64
+    assert bench._pw_ws(bench.CONFIGS[2]) == 4 and bench._pw_ws(bench.CONFIGS[4]) == 4
+    assert bench._pw_ws(bench.CONFIGS[1]) == 8
+
+
+def test_patch_weighted_bytes(bench):
+    N = 1000
+    # (1 + 24 + 20 (24 + 2) + 27) N s with fp64 planes
+    assert bench.algorithmic_bytes("patch_weighted", 1, N) == 572 * N * 8
+    # fp32 planes: N (8 + 24*4 + 20 (24*4 + 16) + 24*4 + 24) = 2464 N = 308 N s
+    assert bench.algorithmic_bytes("patch_weighted", 1, N, ws=4) == 308 * N * 8
+    assert bench.algorithmic_bytes("patch_weighted", 3, N, ws=4) == 3 * 308 * N * 8
+
+
+def test_fourier_and_ve_bytes(bench):
+    B, N, s = 64, 256 * 256, 8
+    assert bench.algorithmic_bytes("row_inv", B, N) == 4 * B * N * s
+    assert bench.algorithmic_bytes("row_fwd", B, N) == 2 * B * N * s
+    assert bench.algorithmic_bytes("gram", B, N) == 7 * B * N * s     # kappa + 2 iterates
+    assert bench.algorithmic_bytes("combine", B, N) == 7 * B * N * s
+    assert bench.algorithmic_bytes("no_such_kernel", B, N) is None
+
+
+def test_filter_bank_flops(bench):
+    # 8 filters x 5x5 correlation + adjoint, FMA = 2 flops
+    assert bench.algorithmic_flops("filter_bank", 2, 100) == 2 * 100 * 8 * 25 * 2 * 2
+    assert bench.algorithmic_flops("row_inv", 2, 100) is None
