@@ -437,6 +437,18 @@ class TestPatchWeightedFp32Planes:
                  R.patch_weighted(x, 1, 2, 60.0, 7))
         assert e2 <= 1e-6
 
+    @pytest.mark.parametrize("wdt", ["float32", "float64"])
+    @pytest.mark.parametrize("shape", [(136, 260), (24, 520), (256, 256), (40, 128)])
+    def test_vector_sweep_vs_oracle(self, rv, R, monkeypatch, wdt, shape):
+        # the vectorised sweep (picked automatically only for large images)
+        monkeypatch.setenv("REDVE_PW_VEC", "1")
+        x = np.random.default_rng(19).uniform(0, 255, shape)
+        got = rv.PatchWeighted(weight_dtype=wdt)(x)
+        assert rel(got, R.patch_weighted(x)) <= (1e-6 if wdt == "float32" else 1e-12)
+        monkeypatch.setenv("REDVE_PW_VEC", "0")
+        scalar = rv.PatchWeighted(weight_dtype=wdt)(x)
+        assert rel(got, scalar) <= 1e-14
+
     def test_generic_radii_keep_fp64(self, rv, R):
         # radii without a compile-time specialisation run the generic fp64 kernels
         x = np.random.default_rng(18).uniform(0, 255, (40, 36))
