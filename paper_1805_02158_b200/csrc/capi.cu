@@ -1050,13 +1050,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   if (ve) {
     CK(p->q.ensure(sizeof(double) * N * kp1 * B));
     size_t need = (size_t)B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2);
-    if (need * sizeof(double) > p->partials.n) {
-      DevBuf tmp;
-      // grow partials (keep row-kernel requirement too)
-      size_t old = p->partials.n;
-      (void)old;
+    if (need * sizeof(double) > p->partials.n)  // grow (the row kernels' share fits inside)
       CK(p->partials.ensure(need * sizeof(double) + 64));
-    }
   }
   // trace buffers (device)
   const size_t nrec = (size_t)B * cap, ncyc = (size_t)B * ccap;
