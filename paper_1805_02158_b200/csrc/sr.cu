@@ -180,6 +180,15 @@ constexpr int PW_ROWS = 4;  // output rows per thread (a column strip), 256 thre
 // keeps the (4+2PR) x (2PR+1) patch of x around it in registers; for each
 // offset it forms the squared differences, the separable box sums and the
 // exponential without any block synchronisation.
+// exp of the (fp64) weight argument in the plane's precision: fp32 planes
+// take the single-precision exp (within 2 fp32 ulp of the rounded fp64 value)
+template <typename WT>
+__device__ __forceinline__ WT pw_weight(double arg);
+template <>
+__device__ __forceinline__ double pw_weight<double>(double arg) { return exp(arg); }
+template <>
+__device__ __forceinline__ float pw_weight<float>(double arg) { return expf((float)arg); }
+
 template <int PR, int SR, typename WT>
 __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
   constexpr int HALO = PR + SR, X = PW_T + 2 * HALO, P = 2 * PR + 1, R = PW_ROWS + 2 * PR;
@@ -229,8 +238,7 @@ __global__ void __launch_bounds__(256) k_pw_weights_t(PwArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < P; ++t) s += rs[m + t];
-      if (m < rows)
-        w0[(long long)k * N + (long long)m * W] = (WT)exp(-fmax(s * inv_box, 0.0) * a.inv_h2);
+      if (m < rows) w0[(long long)k * N + (long long)m * W] = pw_weight<WT>(-fmax(s * inv_box, 0.0) * a.inv_h2);
     }
   }
 }
