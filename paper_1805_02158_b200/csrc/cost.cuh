@@ -46,6 +46,27 @@ __device__ __forceinline__ cd median_cols(const Sorted3& A, const Sorted3& B, co
   return r;
 }
 
+// Medians of two neighbouring 3x3 windows, columns (A, B, C) and (B, C, D):
+// max(B.lo, C.lo), min(B.hi, C.hi) and the ordered pair (B.mid, C.mid) are
+// shared, 3 of the 9 min/max/compare-swaps per output pair (same values as two
+// median_cols calls: every step selects one of its inputs).
+__device__ __forceinline__ void median_pair1(double al, double am, double ah, double bl, double bm,
+                                             double bh, double cl, double cm, double ch, double dl,
+                                             double dm, double dh, double& o0, double& o1) {
+  const double lbc = dmax(bl, cl), hbc = dmin(bh, ch);
+  const double p = dmin(bm, cm), q = dmax(bm, cm);
+  o0 = med3d(dmax(al, lbc), dmax(p, dmin(q, am)), dmin(ah, hbc));
+  o1 = med3d(dmax(lbc, dl), dmax(p, dmin(q, dm)), dmin(hbc, dh));
+}
+
+__device__ __forceinline__ void median_pair(const Sorted3& A, const Sorted3& B, const Sorted3& C,
+                                            const Sorted3& D, cd& r0, cd& r1) {
+  median_pair1(A.lo.x, A.mid.x, A.hi.x, B.lo.x, B.mid.x, B.hi.x, C.lo.x, C.mid.x, C.hi.x, D.lo.x,
+               D.mid.x, D.hi.x, r0.x, r1.x);
+  median_pair1(A.lo.y, A.mid.y, A.hi.y, B.lo.y, B.mid.y, B.hi.y, C.lo.y, C.mid.y, C.hi.y, D.lo.y,
+               D.mid.y, D.hi.y, r0.y, r1.y);
+}
+
 // k x k periodic convolution over the 16 contiguous columns [c0, c0+16) of
 // tile row ti (pairs), K known at compile time.  Same terms and per-output
 // order (ta outer, tb inner) as the runtime loop below.
@@ -90,11 +111,11 @@ __device__ __forceinline__ void denoise_span(cd (&f)[16], const cd* tile, const 
     };
     Sorted3 A = col(-1), B = col(0);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      Sorted3 C = col(j + 1);
-      f[j] = median_cols(A, B, C);
-      A = B;
-      B = C;
+    for (int j = 0; j < 16; j += 2) {
+      Sorted3 C = col(j + 1), D = col(j + 2);
+      median_pair(A, B, C, D, f[j], f[j + 1]);
+      A = C;
+      B = D;
     }
   } else if (DK == DN_CONV && (ksize == 3 || ksize == 5)) {
     // compile-time taps loop: the 16 accumulator chains interleave
@@ -174,10 +195,8 @@ __device__ __forceinline__ void fk_pair(const double* x, int H, int W, int i, in
       c[q][1] = b;
       c[q][2] = e;
     }
-    f0 = med3d(dmax(dmax(c[0][0], c[1][0]), c[2][0]), med3d(c[0][1], c[1][1], c[2][1]),
-               dmin(dmin(c[0][2], c[1][2]), c[2][2]));
-    f1 = med3d(dmax(dmax(c[1][0], c[2][0]), c[3][0]), med3d(c[1][1], c[2][1], c[3][1]),
-               dmin(dmin(c[1][2], c[2][2]), c[3][2]));
+    median_pair1(c[0][0], c[0][1], c[0][2], c[1][0], c[1][1], c[1][2], c[2][0], c[2][1], c[2][2],
+                 c[3][0], c[3][1], c[3][2], f0, f1);
   } else if (DK == DN_CONV && (dn.ksize == 3 || dn.ksize == 5)) {
     if (dn.ksize == 5) conv_pair<5>(x, H, W, i, j, taps, f0, f1);
     else conv_pair<3>(x, H, W, i, j, taps, f0, f1);
