@@ -157,7 +157,9 @@ class NativeSlabOps:
         return self.torch.zeros(shape, dtype=self.torch.float64, device="cuda")
 
     def host(self, t):
-        return t.detach().cpu().numpy()
+        from . import _io
+
+        return _io.host_array(t)
 
     def copy(self, t):
         return t.clone()
