@@ -25,6 +25,7 @@ per step, a process pool over every core.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -259,13 +260,21 @@ def run_reference(a):
 
 # ----------------------------------------------------------------------------- GPU side
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.window = None
+        self.first = ""
+
+    def mark(self, t0, t1):
+        """Wall-clock bounds of the timed region: only samples inside it count
+        (the sampler is started before the warm-up so nvidia-smi's own start-up
+        does not land in the timed region)."""
+        self.window = (t0, t1)
 
     def start(self):
         if os.environ.get("REDVE_BENCH_NO_SMI") == "1":  # diagnostics only
@@ -277,18 +286,37 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        # wait for the first sample: nvidia-smi's start-up (hundreds of ms on a
+        # fresh box) must not overlap the timed region
+        import select
+
+        ready, _, _ = select.select([self.proc.stdout], [], [], 15.0)
+        self.first = self.proc.stdout.readline() if ready else ""
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        out = self.first + out
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in out.strip().splitlines():
             f = [v.strip() for v in line.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            rows.append((ts, f[1:]))
+        if self.window is not None:
+            lo, hi = self.window[0] - 0.15, self.window[1] + 0.15
+            inside = [r for r in rows if r[0] is not None and lo <= r[0] <= hi]
+            rows = inside or rows[-1:]  # a region shorter than the period: the nearest sample
+        for _, f in rows:
             try:
                 sm.append(float(f[0]))
                 smax = float(f[1])
@@ -405,22 +433,24 @@ def run_native(a):
         if world > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(a.warmup):
         batch.solve(x0, cfg)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
-    clocks.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     l0 = nat.kernel_launches()
+    tw0 = time.time()
     e0.record(stream)
     for _ in range(a.steps):
         res = batch.solve(x0, cfg)
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark(tw0, time.time())
     l1 = nat.kernel_launches()
     barrier()
     clk = clocks.stop()
@@ -581,21 +611,23 @@ def run_spatial(a):
         if world > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(a.warmup):
         one_step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     l0 = nat.kernel_launches()
+    tw0 = time.time()
     e0.record(stream)
     for _ in range(a.steps):
         _, tr = one_step()
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark(tw0, time.time())
     l1 = nat.kernel_launches()
     barrier()
     clk = clocks.stop()

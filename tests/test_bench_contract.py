@@ -50,3 +50,32 @@ def test_filter_bank_flops(bench):
     # 8 filters x 5x5 correlation + adjoint, FMA = 2 flops
     assert bench.algorithmic_flops("filter_bank", 2, 100) == 2 * 100 * 8 * 25 * 2 * 2
     assert bench.algorithmic_flops("row_inv", 2, 100) is None
+
+
+def test_clock_sampler_keeps_the_timed_window(bench):
+    import datetime
+    import time
+
+    class FakeProc:
+        def __init__(self, out):
+            self.out = out
+
+        def terminate(self):
+            pass
+
+        def communicate(self, timeout=None):
+            return self.out, None
+
+    def stamp(t):
+        return datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+
+    now = time.time()
+    rows = [(now - 1.0, 1200, "Not Active"), (now, 1965, "Active"), (now + 1.0, 1500, "Not Active")]
+    out = "\n".join(f"{stamp(t)}, {mhz}, 1965, 500.0, 0x0, Not Active, Not Active, Not Active, {cap}"
+                    for t, mhz, cap in rows)
+    c = bench.ClockSampler(0)
+    c.proc = FakeProc(out)
+    c.mark(now - 0.05, now + 0.05)
+    got = c.stop()
+    assert got["sm_mhz"] == 1965.0 and got["samples"] == 1
+    assert got["reasons"] == ["sw_power_cap"]
