@@ -260,24 +260,36 @@ def run_reference(a):
 
 # ----------------------------------------------------------------------------- GPU side
 class ClockSampler:
+    """SM clock and throttle reasons sampled during the timed region.
+
+    NVML (nvidia-ml-py) is polled from a background thread every 20 ms: a
+    cheap query, unlike an ``nvidia-smi -lms`` loop whose start-up and
+    per-sample queries measurably stalled short timed regions (configs[0]:
+    7.5 -> 10.8 ms per step).  nvidia-smi remains the fallback."""
+
     FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    PERIOD = 0.02
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.window = None
         self.first = ""
+        self.thread = None
+        self.samples = []  # (time, sm_mhz, [reason names])
+        self.smax = None
 
     def mark(self, t0, t1):
-        """Wall-clock bounds of the timed region: only samples inside it count
-        (the sampler is started before the warm-up so nvidia-smi's own start-up
-        does not land in the timed region)."""
+        """Wall-clock bounds of the timed region: only samples inside it count."""
         self.window = (t0, t1)
 
     def start(self):
         if os.environ.get("REDVE_BENCH_NO_SMI") == "1":  # diagnostics only
+            return
+        if self._start_nvml():
             return
         try:
             self.proc = subprocess.Popen(
@@ -287,22 +299,71 @@ class ClockSampler:
         except OSError:
             self.proc = None
             return
-        # wait for the first sample: nvidia-smi's start-up (hundreds of ms on a
-        # fresh box) must not overlap the timed region
+        # wait for the first sample: nvidia-smi's start-up must not overlap the timed region
         import select
 
         ready, _, _ = select.select([self.proc.stdout], [], [], 15.0)
         self.first = self.proc.stdout.readline() if ready else ""
 
+    def _start_nvml(self):
+        try:
+            import threading
+
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                                  None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = [(nv.nvmlClocksThrottleReasonHwSlowdown, "hw_slowdown"),
+                    (nv.nvmlClocksThrottleReasonHwThermalSlowdown, "hw_thermal_slowdown"),
+                    (nv.nvmlClocksThrottleReasonSwThermalSlowdown, "sw_thermal_slowdown"),
+                    (nv.nvmlClocksThrottleReasonSwPowerCap, "sw_power_cap")]
+        except Exception:
+            return False
+        self._stop_evt = threading.Event()
+
+        def poll():
+            while not self._stop_evt.is_set():
+                try:
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = get_reasons(h)
+                    self.samples.append((time.time(), mhz, [n for b, n in bits if r & b]))
+                except Exception:
+                    pass
+                self._stop_evt.wait(self.PERIOD)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        while not self.samples and self.thread.is_alive():
+            time.sleep(0.005)
+        return True
+
+    def _in_window(self, rows):
+        if self.window is None:
+            return rows
+        lo, hi = self.window[0] - 0.025, self.window[1] + 0.025
+        inside = [r for r in rows if r[0] is not None and lo <= r[0] <= hi]
+        return inside or rows[-1:]  # a region shorter than the period: the nearest sample
+
+    def _summary(self, rows, smax):
+        sm = [r[1] for r in rows if r[1] is not None]
+        reasons = sorted({n for r in rows for n in r[2]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(sm)}
+
     def stop(self):
+        if self.thread is not None:
+            self._stop_evt.set()
+            self.thread.join(timeout=5)
+            return self._summary(self._in_window(self.samples), self.smax)
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
         out = self.first + out
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        rows = []
+        rows, smax = [], None
         for line in out.strip().splitlines():
             f = [v.strip() for v in line.split(",")]
             if len(f) < 9:
@@ -311,22 +372,13 @@ class ClockSampler:
                 ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
                 ts = None
-            rows.append((ts, f[1:]))
-        if self.window is not None:
-            lo, hi = self.window[0] - 0.15, self.window[1] + 0.15
-            inside = [r for r in rows if r[0] is not None and lo <= r[0] <= hi]
-            rows = inside or rows[-1:]  # a region shorter than the period: the nearest sample
-        for _, f in rows:
             try:
-                sm.append(float(f[0]))
-                smax = float(f[1])
+                mhz, smax = float(f[1]), float(f[2])
             except ValueError:
                 continue
-            for n, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+            rows.append((ts, mhz, [n for n, v in zip(self.NAMES, f[5:9])
+                                   if v.lower().startswith("active")]))
+        return self._summary(self._in_window(rows), smax)
 
 
 def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20, ws=8):
