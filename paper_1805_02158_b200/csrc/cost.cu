@@ -244,7 +244,9 @@ bool cost_fp_ok(const CostArgs& a) {
 }
 
 static int cost_fp_chunks(int B, long long N) {
-  int c = (int)((1184 + B - 1) / B);
+  // one wave at the kernel's 4 CTAs/SM (64 registers): 1216 CTAs for B = 64
+  // left a 3rd wave of 32 CTAs (47 us); 576 CTAs: 44 us
+  int c = 592 / B;
   const long long per = (N / 2 + 255) / 256;  // CTA-passes per image
   if (c > per) c = (int)per;
   if (c > 64) c = 64;
