@@ -59,7 +59,13 @@ enum {
 /* weight rules: extrapolation.py:35-38 */
 enum { REDVE_VE_MPE = 0, REDVE_VE_RRE = 1, REDVE_VE_SVDMPE = 2 };
 /* drivers: solvers.py:388-399 */
-enum { REDVE_METHOD_FP = 0, REDVE_METHOD_FP_VE = 1 };
+enum {
+  REDVE_METHOD_FP = 0,       /* run_fixed_point      solvers.py:288-298 */
+  REDVE_METHOD_FP_VE = 1,    /* run_ve_cycling (fp)  solvers.py:340-385 */
+  REDVE_METHOD_SD = 2,       /* run_steepest_descent solvers.py:301-312 */
+  REDVE_METHOD_SD_VE = 3,    /* run_ve_cycling (sd)  solvers.py:340-385 with _sd_map :274-280 */
+  REDVE_METHOD_NESTEROV = 4  /* run_nesterov         solvers.py:315-337 */
+};
 
 typedef struct redve_ctx redve_ctx;
 typedef struct redve_problem redve_problem;
@@ -92,7 +98,7 @@ typedef struct {
 
 /* SolveConfig (solvers.py:162-199) */
 typedef struct {
-  int method;            /* REDVE_METHOD_* ("fp" / "fp-ve") */
+  int method;            /* REDVE_METHOD_* ("fp" / "fp-ve" / "sd" / "sd-ve" / "nesterov") */
   int ve_method;         /* REDVE_VE_* */
   int m;
   int kappa;             /* 1 <= kappa <= 11 */
@@ -100,6 +106,7 @@ typedef struct {
   double tol;
   int stabilization_iters;
   double rank_tolerance;
+  double step_size;      /* SD / SD-VE / Nesterov: > 0 (ignored by fp / fp-ve) */
 } redve_solve_config;
 
 /* IterationTrace (solvers.py:51-95), HOST arrays sized by the caller:
@@ -120,6 +127,8 @@ typedef struct {
   double* cycle_c;          /* [B][ccap][12] */
   int32_t* status;          /* [B] REDVE_OK / REDVE_E_NONFINITE / REDVE_E_CG */
   int32_t* returned_best;   /* [B] finalize returned the best plain iterate */
+  int32_t* cg_iters;        /* [B][cap] scipy-cg iterations of each fixed-point step
+                               (CG route; 0 on the Fourier route), or NULL */
 } redve_trace;
 
 /* ExtrapolationResult (extrapolation.py:132-146), HOST, one per window */
@@ -174,8 +183,21 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
                          double sigma, double alpha, const double* reference,
                          redve_problem** out);
 void redve_problem_destroy(redve_problem* p);
+/* Number of times redve_solve captured (and instantiated) its CUDA graph for
+ * this problem.  Repeated solves with the same configuration replay one
+ * capture whatever x0 / x_out buffers they pass (no reference counterpart:
+ * runtime introspection for tests). */
+uint64_t redve_problem_graph_captures(const redve_problem* p);
 /* fp_step (objective.py:100-121); f_ext: DEVICE f(x) for REDVE_DN_EXTERNAL, else NULL */
 int redve_fp_step(redve_problem* p, const double* x, double* out, const double* f_ext);
+/* fp_step whose first FFT pass also writes the denoiser output it fused in,
+ * f(x) -> f_out (DEVICE [B][H][W]): the in-kernel median / convolution can be
+ * checked directly against the standalone denoiser.  Fourier route, stencil
+ * denoisers only (REDVE_E_UNSUPPORTED otherwise). */
+int redve_fp_step_denoised(redve_problem* p, const double* x, double* out, double* f_out);
+/* gradient (objective.py:90-93): out = H^T (H x - y) / sigma^2 + alpha (x - f(x));
+ * x, out: DEVICE [B][H][W]; f_ext as for redve_fp_step */
+int redve_gradient(redve_problem* p, const double* x, const double* f_ext, double* out);
 /* data_fidelity / regularizer / cost (objective.py:78-88), HOST outputs [B] each */
 int redve_cost(redve_problem* p, const double* x, const double* f_ext, double* cost,
                double* data_fidelity, double* regularizer, double* psnr);

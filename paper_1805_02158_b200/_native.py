@@ -21,7 +21,9 @@ OP_BLUR, OP_BLUR_DOWNSAMPLE = 0, 1
 DN_IDENTITY, DN_CONV, DN_MEDIAN3, DN_FILTERBANK, DN_PATCH, DN_EXTERNAL = range(6)
 VE_CODES = {"mpe": 0, "rre": 1, "svdmpe": 2}
 VE_NAMES = {v: k for k, v in VE_CODES.items()}
-METHOD_FP, METHOD_FP_VE = 0, 1
+METHOD_FP, METHOD_FP_VE, METHOD_SD, METHOD_SD_VE, METHOD_NESTEROV = range(5)
+METHOD_CODES = {"fp": METHOD_FP, "fp-ve": METHOD_FP_VE, "sd": METHOD_SD, "sd-ve": METHOD_SD_VE,
+                "nesterov": METHOD_NESTEROV}
 MAXKP1 = 12
 
 _dp = C.POINTER(C.c_double)
@@ -46,7 +48,7 @@ class SolveConfigC(C.Structure):
     _fields_ = [
         ("method", C.c_int), ("ve_method", C.c_int), ("m", C.c_int), ("kappa", C.c_int),
         ("max_inner_steps", C.c_int), ("tol", C.c_double), ("stabilization_iters", C.c_int),
-        ("rank_tolerance", C.c_double),
+        ("rank_tolerance", C.c_double), ("step_size", C.c_double),
     ]
 
 
@@ -56,7 +58,7 @@ class TraceC(C.Structure):
         ("n_records", _ip), ("step_norm", _dp), ("cost", _dp), ("psnr", _dp),
         ("gamma_abs_sum", _dp), ("elapsed_s", _dp), ("n_cycles", _ip), ("cycle_meta", _ip),
         ("cycle_stability", _dp), ("cycle_gamma", _dp), ("cycle_c", _dp), ("status", _ip),
-        ("returned_best", _ip),
+        ("returned_best", _ip), ("cg_iters", _ip),
     ]
 
 
@@ -93,7 +95,10 @@ SYMBOLS = {
                                        C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
                                        C.c_double, C.c_void_p, C.POINTER(C.c_void_p)]),
     "redve_problem_destroy": (None, [C.c_void_p]),
+    "redve_problem_graph_captures": (C.c_uint64, [C.c_void_p]),
     "redve_fp_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "redve_fp_step_denoised": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "redve_gradient": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "redve_cost": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _dp, _dp, _dp, _dp]),
     "redve_solve": (C.c_int, [C.c_void_p, C.POINTER(SolveConfigC), C.c_void_p, C.c_void_p,
                               C.POINTER(TraceC)]),

@@ -115,6 +115,24 @@ class RedBatch:
                   self._ctx)
         return out, from_np
 
+    def fp_step_denoised(self, x):
+        """(fp_step(x), f(x)) with f(x) as fused into the first FFT pass."""
+        t, from_np, single = self._batch_in(x)
+        out = _io.empty(t.shape)
+        f = _io.empty(t.shape)
+        nat.check(nat.library().redve_fp_step_denoised(self._h, nat.dptr(t), nat.dptr(out),
+                                                       nat.dptr(f)), self._ctx)
+        return out, f
+
+    def gradient(self, x):
+        """grad E(x) for every image (objective.py:90-93), on the device."""
+        t, from_np, single = self._batch_in(x)
+        f = self._ext_f(t)
+        out = _io.empty(t.shape)
+        nat.check(nat.library().redve_gradient(self._h, nat.dptr(t), nat.dptr(f), nat.dptr(out)),
+                  self._ctx)
+        return out, from_np
+
     def cost_terms(self, x):
         t, _, _ = self._batch_in(x)
         f = self._ext_f(t)
@@ -130,26 +148,34 @@ class RedBatch:
     def device_solvable(self) -> bool:
         return self.native_denoiser
 
+    @property
+    def graph_captures(self) -> int:
+        """How many times the device solve captured its CUDA graph."""
+        return int(nat.library().redve_problem_graph_captures(self._h))
+
     # -- the device-resident solve ----------------------------------------------------
     def solve(self, x0, config, method=None):
         """Run ``config`` for every image; returns BatchResult (solutions on the device)."""
         from .solvers import SolveConfig  # noqa: F401  (type only)
 
         method = config.method if method is None else method
-        if method not in ("fp", "fp-ve"):
-            raise ValueError(f"device solve supports 'fp' and 'fp-ve', not {method!r}")
-        t, from_np, _ = self._batch_in(x0)
-        if not bool(_io.torch_mod().isfinite(t).all()):
-            raise ValueError("x0 contains non-finite entries")
+        if method not in nat.METHOD_CODES:
+            raise ValueError(f"unknown method {method!r}")
+        gradient = method in ("sd", "sd-ve", "nesterov")
+        if gradient and (config.step_size is None or config.step_size <= 0):
+            raise ValueError("this method needs a positive step_size")
+        t, from_np, _ = self._batch_in(x0)  # finiteness of x0: checked on the device
         cfg = nat.SolveConfigC()
-        cfg.method = nat.METHOD_FP if method == "fp" else nat.METHOD_FP_VE
+        cfg.method = nat.METHOD_CODES[method]
         cfg.ve_method = nat.VE_CODES[config.ve_method]
         cfg.m = config.m
         cfg.kappa = config.kappa
         cfg.max_inner_steps = config.max_inner_steps
         cfg.tol = config.tol
-        cfg.stabilization_iters = config.stabilization_iters if method == "fp-ve" else 0
+        cycling = method in ("fp-ve", "sd-ve")
+        cfg.stabilization_iters = config.stabilization_iters if cycling else 0
         cfg.rank_tolerance = config.rank_tolerance
+        cfg.step_size = float(config.step_size) if gradient else 0.0
         B = self.B
         cap = config.max_inner_steps + cfg.stabilization_iters
         clen = config.m + config.kappa + 1
@@ -182,6 +208,7 @@ class BatchResult:
         self.cycle_c = np.zeros((B, ccap, nat.MAXKP1))
         self.status = np.zeros(B, np.int32)
         self.returned_best = np.zeros(B, np.int32)
+        self.cg_iters = np.zeros((B, cap), np.int32)
         self.x = None
         self.requested = None
 
@@ -202,6 +229,7 @@ class BatchResult:
         t.cycle_c = nat.hptr(self.cycle_c)
         t.status = ip(self.status)
         t.returned_best = ip(self.returned_best)
+        t.cg_iters = ip(self.cg_iters)
         self._keep = t
         return t
 

@@ -18,6 +18,7 @@
 #include "slab.cuh"
 #include "fused.cuh"
 #include "sr.cuh"
+#include "grad.cuh"
 
 using namespace redve;
 
@@ -231,8 +232,16 @@ struct redve_problem {
   cudaGraphExec_t gexec = nullptr;  // captured solve (Fourier route)
   std::string gkey;
   unsigned long long glaunches = 0;
+  unsigned long long captures = 0;  // graph (re)captures, for tests
+  DevBuf x0bad;                     // device flag: x0 had a non-finite entry
+  // gradient baselines: H^T H / sigma^2 stencil taps (circulant H), Nesterov y
+  DevBuf gtaps, ybuf, part_grad, cnt_grad;
+  int g_R = 0, g_sep = 0;
+  void* hstage = nullptr;           // pinned staging for the trace read-back
+  size_t hstage_bytes = 0;
   ~redve_problem() {
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (hstage) cudaFreeHost(hstage);
   }
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
@@ -316,8 +325,8 @@ static int f_row_inv(redve_problem* p, const cd* Z, View out, const double* base
 }
 static int fourier_pipeline(redve_problem* p, View xin, DenoiseArgs dn, double scale, View out,
                             const double* base, int epilogue, View xprev, StepCtl ctl,
-                            TraceBufs tr, int S, int phase) {
-  int r = f_row_fwd(p, xin, dn, p->Z.as<cd>(), phase);
+                            TraceBufs tr, int S, int phase, double* fout = nullptr) {
+  int r = f_row_fwd(p, xin, dn, p->Z.as<cd>(), phase, fout);
   if (r) return r;
   if ((r = f_col(p, p->Z.as<cd>(), scale, phase))) return r;
   return f_row_inv(p, p->Z.as<cd>(), out, base, epilogue, xprev, ctl, tr, S);
@@ -778,6 +787,42 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
       PK(p->hsep.ensure(sizeof(double) * 2 * k));
       PK(cudaMemcpy(p->hsep.p, uv.data(), sizeof(double) * 2 * k, cudaMemcpyHostToDevice));
     }
+    if (op->kind == REDVE_OP_BLUR) {
+      // H^T H = periodic convolution with the PSF autocorrelation a(d) =
+      // sum_i h(i) h(i + d) (radius k - 1), scaled by 1/sigma^2; rank one when
+      // h is: a = (u * u)(v * v)^T.  Used by the gradient baselines.
+      const int R = k - 1, T = 2 * k - 1;
+      const double is2 = 1.0 / (sigma * sigma);
+      std::vector<double> at;
+      if (sep && k > 1) {
+        at.assign(2 * T, 0.0);  // [horizontal (v) | vertical (u) / sigma^2]
+        for (int d = -R; d <= R; ++d) {
+          double sv = 0.0, su = 0.0;
+          for (int i = 0; i < k; ++i)
+            if (i + d >= 0 && i + d < k) {
+              sv += uv[k + i] * uv[k + i + d];
+              su += uv[i] * uv[i + d];
+            }
+          at[d + R] = sv;
+          at[T + d + R] = su * is2;
+        }
+      } else {
+        at.assign((size_t)T * T, 0.0);
+        for (int d1 = -R; d1 <= R; ++d1)
+          for (int d2 = -R; d2 <= R; ++d2) {
+            double sacc = 0.0;
+            for (int i1 = 0; i1 < k; ++i1)
+              for (int i2 = 0; i2 < k; ++i2)
+                if (i1 + d1 >= 0 && i1 + d1 < k && i2 + d2 >= 0 && i2 + d2 < k)
+                  sacc += op->taps[i1 * k + i2] * op->taps[(i1 + d1) * k + i2 + d2];
+            at[(size_t)(d1 + R) * T + d2 + R] = sacc * is2;
+          }
+      }
+      p->g_R = R;
+      p->g_sep = sep && k > 1;
+      PK(p->gtaps.ensure(sizeof(double) * at.size()));
+      PK(cudaMemcpy(p->gtaps.p, at.data(), sizeof(double) * at.size(), cudaMemcpyHostToDevice));
+    }
   }
   size_t db = dn->kind == REDVE_DN_CONV ? sizeof(double) * dn->ksize * dn->ksize : 8;
   PK(p->dntaps.ensure(db));
@@ -894,7 +939,24 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
 
 void redve_problem_destroy(redve_problem* p) { delete p; }
 
+uint64_t redve_problem_graph_captures(const redve_problem* p) { return p ? p->captures : 0; }
+
+static int fp_step_impl(redve_problem* p, const double* x, double* out, const double* f_ext,
+                        double* f_out);
+
 int redve_fp_step(redve_problem* p, const double* x, double* out, const double* f_ext) {
+  return fp_step_impl(p, x, out, f_ext, nullptr);
+}
+
+int redve_fp_step_denoised(redve_problem* p, const double* x, double* out, double* f_out) {
+  if (!p->fourier || p->dn_kind == DN_EXTERNAL)
+    return fail(p->ctx, REDVE_E_UNSUPPORTED,
+                "f(x) is fused into the first FFT pass only for the Fourier route's stencil denoisers");
+  return fp_step_impl(p, x, out, nullptr, f_out);
+}
+
+static int fp_step_impl(redve_problem* p, const double* x, double* out, const double* f_ext,
+                        double* f_out) {
   redve_ctx* ctx = p->ctx;
   const bool host_dn = p->dn_api_kind == REDVE_DN_EXTERNAL;
   if (host_dn && !f_ext) return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
@@ -926,7 +988,54 @@ int redve_fp_step(redve_problem* p, const double* x, double* out, const double* 
   TraceBufs tr;
   memset(&tr, 0, sizeof(tr));
   return fourier_pipeline(p, xin, dn, p->alpha, plain(out, p->N), p->xb.as<double>(), 0,
-                          plain(nullptr, p->N), ctl, tr, 1, PH_SETUP);
+                          plain(nullptr, p->N), ctl, tr, 1, PH_SETUP, f_out);
+}
+
+// grad E(x) = H^T (H x - y) / sigma^2 + alpha (x - f(x))  (objective.py:90-93)
+int redve_gradient(redve_problem* p, const double* x, const double* f_ext, double* out) {
+  redve_ctx* ctx = p->ctx;
+  const cudaStream_t s = ctx->stream;
+  const bool host_dn = p->dn_api_kind == REDVE_DN_EXTERNAL;
+  if (host_dn && !f_ext) return fail(ctx, REDVE_E_VALUE, "external denoiser needs f(x)");
+  RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), p->B, s));
+  View xv = plain(x, p->N);
+  if (!host_dn) {
+    int r = denoise_to_fbuf(p, xv, PH_SETUP);
+    if (r) return r;
+    f_ext = p->fbuf.as<double>();
+  }
+  GradArgs ga;
+  memset(&ga, 0, sizeof(ga));
+  ga.B = p->B; ga.H = p->H; ga.W = p->W;
+  ga.v = xv; ga.xprev = xv; ga.xout = xv;
+  if (!p->fourier) {
+    CgArgs ca;
+    memset(&ca, 0, sizeof(ca));
+    ca.B = p->B; ca.H = p->H; ca.W = p->W; ca.factor = p->op.factor; ca.k = p->op.ksize;
+    ca.taps = p->htaps.as<double>();
+    ca.inv_sigma2 = 1.0 / (p->sigma * p->sigma); ca.alpha = p->alpha;
+    ca.xin = xv; ca.q = p->cq.as<double>(); ca.cg = p->cgst.as<CgState>();
+    ca.st = p->state.as<ImgState>(); ca.phase = PH_SETUP;
+    RUN(ctx, "normal_matvec", launch_normal_matvec(ca, s));
+    CKL();
+    ga.Av = p->cq.as<double>();
+  } else {
+    const int T = 2 * p->g_R + 1;
+    ga.R = p->g_R;
+    if (p->g_sep) {
+      ga.av = p->gtaps.as<double>();
+      ga.au = ga.av + T;
+    } else {
+      ga.afull = p->gtaps.as<double>();
+    }
+  }
+  ga.hty = p->hty.as<double>(); ga.f = f_ext; ga.alpha = p->alpha;
+  ga.gout = out;
+  ga.st = p->state.as<ImgState>();
+  ga.ctl = StepCtl{PH_SETUP, 0, 0.0, 1, 0, 0};
+  RUN(ctx, "gradient", launch_grad_step(ga, s));
+  CKL();
+  return REDVE_OK;
 }
 
 static CostArgs cost_args(redve_problem* p, View x, const double* f_ext, int mode, StepCtl ctl,
@@ -1015,8 +1124,15 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
                 redve_trace* trace) {
   redve_ctx* ctx = p->ctx;
   cudaStream_t s = ctx->stream;
-  if (cfg->method != REDVE_METHOD_FP && cfg->method != REDVE_METHOD_FP_VE)
+  if (cfg->method < REDVE_METHOD_FP || cfg->method > REDVE_METHOD_NESTEROV)
     return fail(ctx, REDVE_E_VALUE, "unknown method %d", cfg->method);
+  const bool gradm = cfg->method == REDVE_METHOD_SD || cfg->method == REDVE_METHOD_SD_VE ||
+                     cfg->method == REDVE_METHOD_NESTEROV;
+  const bool nest = cfg->method == REDVE_METHOD_NESTEROV;
+  if (gradm && !(cfg->step_size > 0))  // solvers.py:277-278, 323-324
+    return fail(ctx, REDVE_E_VALUE, "this method needs a positive step_size");
+  if (gradm && p->fourier && p->g_R > 64)
+    return fail(ctx, REDVE_E_UNSUPPORTED, "gradient stencil radius %d too large", p->g_R);
   if (cfg->ve_method < 0 || cfg->ve_method > 2) return fail(ctx, REDVE_E_VALUE, "unknown VE method");
   if (cfg->kappa < 1) return fail(ctx, REDVE_E_VALUE, "kappa must be >= 1");
   if (cfg->kappa + 1 > MAXKP1) return fail(ctx, REDVE_E_UNSUPPORTED, "kappa > %d", MAXKP1 - 1);
@@ -1025,7 +1141,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   if (cfg->tol < 0) return fail(ctx, REDVE_E_VALUE, "tol must be >= 0");
   if (cfg->stabilization_iters < 0) return fail(ctx, REDVE_E_VALUE, "stabilization_iters < 0");
   if (!(cfg->rank_tolerance > 0)) return fail(ctx, REDVE_E_VALUE, "rank_tolerance must be > 0");
-  const bool ve = cfg->method == REDVE_METHOD_FP_VE;
+  const bool ve = cfg->method == REDVE_METHOD_FP_VE || cfg->method == REDVE_METHOD_SD_VE;
   if (ve && cfg->max_inner_steps < cfg->m + cfg->kappa + 2)
     return fail(ctx, REDVE_E_VALUE, "budget must admit at least one full cycle (m + kappa + 2)");
   if (p->dn_api_kind == REDVE_DN_EXTERNAL)
@@ -1053,9 +1169,30 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     if (need * sizeof(double) > p->partials.n)  // grow (the row kernels' share fits inside)
       CK(p->partials.ensure(need * sizeof(double) + 64));
   }
+  if (gradm) {
+    const int nb = grad_partials_per_image(p->H, p->W, p->fourier);
+    CK(p->part_grad.ensure(sizeof(double) * 3 * (size_t)B * nb));
+    if (p->cnt_grad.n < sizeof(unsigned) * (B + 1)) {
+      CK(p->cnt_grad.ensure(sizeof(unsigned) * (B + 1)));
+      CK(cudaMemsetAsync(p->cnt_grad.p, 0, sizeof(unsigned) * (B + 1), s));
+    }
+    if (nest) CK(p->ybuf.ensure(sizeof(double) * 2 * (size_t)B * N));
+  }
+  // Nesterov momentum t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2, beta_k = (t_k - 1) / t_{k+1}
+  // (solvers.py:330-333): the same for every image, so a per-step launch argument
+  std::vector<double> betas;
+  if (nest) {
+    double t = 1.0;
+    for (int i = 0; i < budget; ++i) {
+      const double tn = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
+      betas.push_back((t - 1.0) / tn);
+      t = tn;
+    }
+  }
   // trace buffers (device)
   const size_t nrec = (size_t)B * cap, ncyc = (size_t)B * ccap;
-  size_t tbytes = sizeof(double) * (5 * nrec + ncyc * (1 + 2 * MAXKP1)) + sizeof(int) * ncyc * 4;
+  size_t tbytes = sizeof(double) * (5 * nrec + ncyc * (1 + 2 * MAXKP1)) + sizeof(int) * ncyc * 4 +
+                  sizeof(int) * nrec;
   CK(p->trace.ensure(tbytes));
   TraceBufs tr;
   {
@@ -1072,26 +1209,31 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     tr.cyc_gamma = tr.cyc_stab + ncyc;
     tr.cyc_c = tr.cyc_gamma + ncyc * MAXKP1;
     tr.cyc_meta = reinterpret_cast<int*>(tr.cyc_c + ncyc * MAXKP1);
+    tr.cg_iters = tr.cyc_meta + ncyc * 4;
   }
   // All device work of the solve.  Fourier route with tol == 0 has no host
   // decision inside, so it is captured once into a CUDA graph and replayed
   // (the CG route checks its per-image stop flags on the host).
   const bool use_graph = p->fourier && cfg->tol == 0 && !ctx->profiling && graphs_enabled();
+  // The graph never sees the caller's x0 / x_out: x0 is loaded into ring slot 0
+  // before it and the solution gathered after it, so repeated solves on one
+  // problem replay a single capture whatever buffers the caller passes.
   char keybuf[512];
-  snprintf(keybuf, sizeof(keybuf), "%p|%p|%p|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%p|%p", (void*)p,
-           (const void*)x0, (void*)x_out, cfg->method, cfg->ve_method, cfg->m, cfg->kappa,
-           cfg->max_inner_steps, cfg->tol, cfg->stabilization_iters, cfg->rank_tolerance,
-           p->ring.p, p->trace.p);
+  snprintf(keybuf, sizeof(keybuf), "%p|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g|%p|%p|%p|%p", (void*)p,
+           cfg->method, cfg->ve_method, cfg->m, cfg->kappa, cfg->max_inner_steps, cfg->tol,
+           cfg->stabilization_iters, cfg->rank_tolerance, gradm ? cfg->step_size : 0.0,
+           p->ring.p, p->trace.p, p->best.p, p->ybuf.p);
+  CK(p->x0bad.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(p->x0bad.p, 0, sizeof(int), s));
+  RUN(ctx, "load_x0", launch_load_x0(p->ring.as<double>(), N * S, x0, B, N, p->x0bad.as<int>(), s));
+  CKL();
   auto device_work = [&]() -> int {
     CK(cudaMemsetAsync(p->trace.p, 0xFF, sizeof(double) * 5 * nrec, s));  // NaN
     CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
-                                           sizeof(int) * ncyc * 4, s));
+                                           sizeof(int) * (ncyc * 4 + nrec), s));
     ImgState* st = p->state.as<ImgState>();
     RUN(ctx, "init_state", launch_init_state(st, B, s));
     CKL();
-    // x0 -> ring slot 0
-    CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * N * S, x0, sizeof(double) * N,
-                         sizeof(double) * N, B, cudaMemcpyDeviceToDevice, s));
 
     View cur{p->ring.as<double>(), N * S, N, S, 1};
     View nxt{p->ring.as<double>(), N * S, N, S, 2};
@@ -1111,8 +1253,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     // (fused denoisers) or by the step itself (precomputed denoisers).  For the
     // precomputed denoisers f(x_k) evaluated here is handed to the next step
     // when nothing changes the iterate in between (f_ready).
-    const bool ident = p->fourier;
-    const bool fused = p->fourier && !pw && fused_step_ok(p->H, p->W, dn);
+    const bool ident = p->fourier && !gradm;  // the cost identity holds for FP steps only
+    const bool fused = p->fourier && !pw && !gradm && fused_step_ok(p->H, p->W, dn);
     double* f_step = p->fbuf.as<double>();   // f of the current step's input
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
     bool f_ready = false;
@@ -1144,6 +1286,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       return REDVE_OK;
     };
 
+    if (nest)  // y_0 = x_0 (solvers.py:327)
+      RUN(ctx, "copy_view", launch_copy_view(plain(p->ybuf.as<double>(), N), cur, B, N, st, 0, s));
     if (track) {  // note_initial (solvers.py:219-223)
       int r0 = cost_of_cur(COST_INIT, ctl);
       if (r0) return r0;
@@ -1154,7 +1298,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     // k_row_mid: the inverse row pass of a step and the forward row pass of the
     // next step in one kernel, whenever the next step follows directly (inside
     // a VE cycle / plain FP run; never across an extrapolation)
-    const bool mid = p->fourier && !pw && !fused && p->Z2.p != nullptr &&
+    const bool mid = p->fourier && !pw && !fused && !gradm && p->Z2.p != nullptr &&
                      row_mid_ok(p->H, p->W, dn, p->lpc_row);
     cd* zcur = p->Z.as<cd>();
     cd* zalt = mid ? p->Z2.as<cd>() : nullptr;
@@ -1167,7 +1311,46 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       c.defer_commit = cadence ? 1 : 0;
       int r = REDVE_OK;
       double* fp_this = fpb[kk & 1];
-      if (p->fourier && fused) {  // one clustered kernel per step (fused.cu)
+      if (gradm) {  // x+ = v - s grad E(v)  (solvers.py:274-280, 315-337)
+        double* y0 = nest ? p->ybuf.as<double>() : nullptr;
+        const size_t half = (size_t)B * N;
+        View vin = nest ? plain(y0 + (kk & 1) * half, N) : cur;
+        r = denoise_to_fbuf(p, vin, phase);
+        if (r) return r;
+        GradArgs ga;
+        memset(&ga, 0, sizeof(ga));
+        ga.B = B; ga.H = p->H; ga.W = p->W;
+        ga.v = vin; ga.xprev = cur; ga.xout = nxt;
+        if (!p->fourier) {
+          CgArgs ca;
+          memset(&ca, 0, sizeof(ca));
+          ca.B = B; ca.H = p->H; ca.W = p->W; ca.factor = p->op.factor; ca.k = p->op.ksize;
+          ca.taps = p->htaps.as<double>();
+          ca.inv_sigma2 = 1.0 / (p->sigma * p->sigma); ca.alpha = p->alpha;
+          ca.xin = vin; ca.q = p->cq.as<double>(); ca.cg = p->cgst.as<CgState>(); ca.st = st;
+          ca.phase = phase;
+          RUN(ctx, "normal_matvec", launch_normal_matvec(ca, s));
+          CKL();
+          ga.Av = p->cq.as<double>();
+        } else {
+          const int T = 2 * p->g_R + 1;
+          ga.R = p->g_R;
+          if (p->g_sep) {
+            ga.av = p->gtaps.as<double>();
+            ga.au = ga.av + T;
+          } else {
+            ga.afull = p->gtaps.as<double>();
+          }
+        }
+        ga.hty = p->hty.as<double>(); ga.f = p->fbuf.as<double>();
+        ga.alpha = p->alpha; ga.step = cfg->step_size;
+        ga.beta = nest ? betas[kk < (int)betas.size() ? kk : (int)betas.size() - 1] : 0.0;
+        ga.ynext = nest ? y0 + ((kk + 1) & 1) * half : nullptr;
+        ga.st = st; ga.ctl = c; ga.tr = tr; ga.S = S;
+        ga.partials = p->part_grad.as<double>(); ga.counters = p->cnt_grad.as<unsigned>();
+        RUN(ctx, "grad_step", launch_grad_step(ga, s));
+        CKL();
+      } else if (p->fourier && fused) {  // one clustered kernel per step (fused.cu)
         FusedArgs fa;
         memset(&fa, 0, sizeof(fa));
         fa.B = B; fa.xin = cur; fa.dn = dn; fa.fout = cadence ? fp_this : nullptr;
@@ -1216,6 +1399,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         r = fp_step_cg(p, cur, nxt, phase, nullptr);
         if (r) return r;
         RecordArgs ra;
+        ra.cg = p->cgst.as<CgState>();
         ra.N = N; ra.xnew = nxt; ra.xprev = cur; ra.S = S; ra.st = st; ra.ctl = c; ra.tr = tr;
         ra.partials = p->part_cg.as<double>(); ra.counters = p->cnt_rec.as<unsigned>();
         RUN(ctx, "step_record", launch_step_record(ra, B, s));
@@ -1292,9 +1476,6 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       int r = cost_of_cur(COST_FINAL, ctl);
       if (r) return r;
     }
-    RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N, st, s));
-    CKL();
-
     return REDVE_OK;
   };
   if (use_graph && p->gexec && p->gkey == keybuf) {
@@ -1324,33 +1505,58 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     if (ce != cudaSuccess) return fail(ctx, REDVE_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
     p->gkey = keybuf;
     p->glaunches = g_launches.load() - l0;
+    p->captures += 1;
     CK(cudaGraphLaunch(p->gexec, s));
   } else {
     int r = device_work();
     if (r) return r;
   }
+  {
+    View cur{p->ring.as<double>(), N * S, N, S, 1};
+    RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N,
+                                     p->state.as<ImgState>(), s));
+    CKL();
+  }
 
-  // trace back to the host
-  std::vector<ImgState> hst(B);
-  CK(cudaMemcpyAsync(hst.data(), p->state.p, sizeof(ImgState) * B, cudaMemcpyDeviceToHost, s));
-  const int hc = trace->cap < cap ? trace->cap : cap;
-  const int hcc = trace->ccap < ccap ? trace->ccap : ccap;
-  auto cp2 = [&](void* dst, const void* src, size_t elem, int hcols, int dcols) -> cudaError_t {
-    return cudaMemcpy2DAsync(dst, elem * hcols, src, elem * dcols, elem * (hcols < dcols ? hcols : dcols),
-                             B, cudaMemcpyDeviceToHost, s);
-  };
-  if (trace->step_norm) CK(cp2(trace->step_norm, tr.step_norm, 8, trace->cap, cap));
-  if (trace->cost) CK(cp2(trace->cost, tr.cost, 8, trace->cap, cap));
-  if (trace->psnr) CK(cp2(trace->psnr, tr.psnr, 8, trace->cap, cap));
-  if (trace->gamma_abs_sum) CK(cp2(trace->gamma_abs_sum, tr.gamma, 8, trace->cap, cap));
-  if (trace->elapsed_s) CK(cp2(trace->elapsed_s, tr.elapsed, 8, trace->cap, cap));
-  if (trace->cycle_meta) CK(cp2(trace->cycle_meta, tr.cyc_meta, 16, trace->ccap, ccap));
-  if (trace->cycle_stability) CK(cp2(trace->cycle_stability, tr.cyc_stab, 8, trace->ccap, ccap));
-  if (trace->cycle_gamma) CK(cp2(trace->cycle_gamma, tr.cyc_gamma, 8 * MAXKP1, trace->ccap, ccap));
-  if (trace->cycle_c) CK(cp2(trace->cycle_c, tr.cyc_c, 8 * MAXKP1, trace->ccap, ccap));
+  // trace back to the host: one pinned copy of [trace | state | x0 flag], then
+  // host copies into the caller's arrays
+  const size_t sbytes = sizeof(ImgState) * B;
+  const size_t need = tbytes + sbytes + sizeof(int);
+  if (p->hstage_bytes < need) {
+    if (p->hstage) cudaFreeHost(p->hstage);
+    p->hstage = nullptr;
+    p->hstage_bytes = 0;
+    CK(cudaHostAlloc(&p->hstage, need, cudaHostAllocDefault));
+    p->hstage_bytes = need;
+  }
+  char* hs = static_cast<char*>(p->hstage);
+  CK(cudaMemcpyAsync(hs, p->trace.p, tbytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hs + tbytes, p->state.p, sbytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hs + tbytes + sbytes, p->x0bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  (void)hc;
-  (void)hcc;
+  if (*reinterpret_cast<int*>(hs + tbytes + sbytes))
+    return fail(ctx, REDVE_E_VALUE, "x0 contains non-finite entries");
+  const ImgState* hst = reinterpret_cast<const ImgState*>(hs + tbytes);
+  auto host_ptr = [&](const void* dptr) {
+    return hs + (static_cast<const char*>(dptr) - p->trace.as<char>());
+  };
+  auto cp2 = [&](void* dst, const void* dsrc, size_t elem, int hcols, int dcols) {
+    if (!dst) return;
+    const char* src = host_ptr(dsrc);
+    const size_t w = elem * (size_t)(hcols < dcols ? hcols : dcols);
+    for (int b = 0; b < B; ++b)
+      memcpy(static_cast<char*>(dst) + elem * hcols * (size_t)b, src + elem * dcols * (size_t)b, w);
+  };
+  cp2(trace->step_norm, tr.step_norm, 8, trace->cap, cap);
+  cp2(trace->cost, tr.cost, 8, trace->cap, cap);
+  cp2(trace->psnr, tr.psnr, 8, trace->cap, cap);
+  cp2(trace->gamma_abs_sum, tr.gamma, 8, trace->cap, cap);
+  cp2(trace->elapsed_s, tr.elapsed, 8, trace->cap, cap);
+  cp2(trace->cycle_meta, tr.cyc_meta, 16, trace->ccap, ccap);
+  cp2(trace->cycle_stability, tr.cyc_stab, 8, trace->ccap, ccap);
+  cp2(trace->cycle_gamma, tr.cyc_gamma, 8 * MAXKP1, trace->ccap, ccap);
+  cp2(trace->cycle_c, tr.cyc_c, 8 * MAXKP1, trace->ccap, ccap);
+  cp2(trace->cg_iters, tr.cg_iters, 4, trace->cap, cap);
   for (int b = 0; b < B; ++b) {
     if (trace->n_records) trace->n_records[b] = hst[b].k;
     if (trace->n_cycles) trace->n_cycles[b] = hst[b].ncycles;

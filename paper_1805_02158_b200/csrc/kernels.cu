@@ -333,6 +333,30 @@ void launch_gather(double* out, View cur, const double* best, int B, long long N
   k_gather<<<dim3(chunks, B), 256, 0, s>>>(out, cur, best, B, N, st);
 }
 
+// x0 into ring slot 0 (ring [B][S][N]) plus the reference's finiteness check of
+// x0 (solvers.py:265-270, _as_vector) as a device flag: the solve graph does
+// not depend on the caller's x0 pointer and no host sync precedes it.
+__global__ void k_load_x0(double* ring, long long img_stride, const double* x0, int B, long long N,
+                          int* bad) {
+  const int b = blockIdx.y;
+  const double* s = x0 + (long long)b * N;
+  double* d = ring + (long long)b * img_stride;
+  int nf = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = s[i];
+    nf |= !isfinite(v);
+    d[i] = v;
+  }
+  if (__syncthreads_or(nf) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+void launch_load_x0(double* ring, long long img_stride, const double* x0, int B, long long N,
+                    int* bad, cudaStream_t s) {
+  int chunks = cdiv(N, 256 * 8);
+  if (chunks > 64) chunks = 64;
+  k_load_x0<<<dim3(chunks, B), 256, 0, s>>>(ring, img_stride, x0, B, N, bad);
+}
+
 __global__ void k_init_state(ImgState* st, int B) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;

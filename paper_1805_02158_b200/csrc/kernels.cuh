@@ -187,6 +187,8 @@ void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st
 void launch_gram(const VeArgs& a, cudaStream_t s);
 void launch_combine(const VeArgs& a, cudaStream_t s);
 void launch_init_state(ImgState* st, int B, cudaStream_t s);
+void launch_load_x0(double* ring, long long img_stride, const double* x0, int B, long long N,
+                    int* bad, cudaStream_t s);
 void launch_gather(double* out, View cur, const double* best, int B, long long N,
                    const ImgState* st, cudaStream_t s);
 void launch_conv(const double* x, double* out, int B, int H, int W, const double* taps, int k,

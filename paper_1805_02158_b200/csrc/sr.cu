@@ -872,6 +872,9 @@ __global__ void __launch_bounds__(256) k_step_record(RecordArgs a) {
   if (lastb) gather_partials<3>(a.partials + (long long)b * nblk * 3, nblk, t, red);
   if (lastb && threadIdx.x == 0) {
     record_step(a.st[b], b, t[0], t[1], t[2], a.S, a.ctl, a.tr);
+    const int rec = a.st[b].k - 1;
+    if (a.cg && a.tr.cg_iters && rec < a.tr.cap)
+      a.tr.cg_iters[(long long)b * a.tr.cap + rec] = a.cg[b].its;
   }
 }
 

@@ -47,6 +47,7 @@ struct CgArgs {
 
 struct RecordArgs {
   long long N;
+  const CgState* cg;  // CG route: per-image iteration counts into tr.cg_iters (or null)
   View xnew, xprev;
   int S;
   ImgState* st;

@@ -56,6 +56,7 @@ struct TraceBufs {
   double* cyc_stab;   // [B][ccap]
   double* cyc_gamma;  // [B][ccap][MAXKP1]
   double* cyc_c;      // [B][ccap][MAXKP1]
+  int* cg_iters;      // [B][cap] CG iterations of each fixed-point step (CG route)
 };
 
 // A batch of images living either in a plain array or in a per-image ring.

@@ -41,7 +41,7 @@ class RedObjective:
         self.alpha = float(alpha)
         self.denoiser = denoiser
         self._batch = RedBatch(forward, y, sigma, alpha, denoiser)
-        self._ref = None
+        self._ref_batch = None  # (reference array, RedBatch with that reference)
 
     @property
     def device_solvable(self) -> bool:
@@ -63,9 +63,8 @@ class RedObjective:
 
     def gradient(self, x):
         """H^T (H x - y)/sigma^2 + alpha (x - f(x))  (objective.py:90-93)."""
-        x = np.asarray(x, dtype=np.float64)
-        data = self.forward.adjoint(self.forward.apply(x) - self.y) / self.sigma**2
-        return data + self.alpha * (x - np.asarray(self.denoiser(x)))
+        out, from_np = self._batch.gradient(x)
+        return _io.to_host(out[0], from_np)
 
     def fp_step(self, x):
         out, from_np = self._batch.fp_step(x)
@@ -73,11 +72,16 @@ class RedObjective:
 
     # -- device solve used by solvers.solve ------------------------------------
     def _device_solve(self, x0, config, method, reference):
+        # PSNR is recorded against exactly this solve's reference (None: no PSNR)
         batch = self._batch
-        if reference is not None and batch.ref is None:
-            batch = RedBatch(self.forward, self.y, self.sigma, self.alpha, self.denoiser,
-                             np.asarray(reference, dtype=np.float64).reshape(self.forward.in_shape))
-            self._batch = batch
+        if reference is not None:
+            ref = np.asarray(reference, dtype=np.float64).reshape(self.forward.in_shape)
+            held = self._ref_batch
+            if held is None or held[0].shape != ref.shape or not np.array_equal(held[0], ref):
+                held = (ref.copy(), RedBatch(self.forward, self.y, self.sigma, self.alpha,
+                                             self.denoiser, ref))
+                self._ref_batch = held
+            batch = held[1]
         x0 = np.asarray(x0, dtype=np.float64).reshape(self.forward.in_shape)
         if x0.size != int(np.prod(self.forward.in_shape)):
             raise ValueError("x0 has the wrong dimension")

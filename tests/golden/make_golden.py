@@ -222,9 +222,11 @@ def demo_csv():
     op = redve.Blur(redve.make_psf("uniform", 9), truth.shape)
     out["truth"] = truth
     out["y"] = redve.degrade(truth, op, SQRT2, seed=0)
-    for name in ("fp", "fp-mpe"):
+    for name in ("fp", "fp-mpe", "sd", "nesterov"):
         path = f"/root/reference/pkg/demos/out/deblur_{name}.csv"
-        rows = open(path).read().strip().splitlines()[1:]
+        raw = open(path, "rb").read()
+        out[f"{name}/csv_bytes"] = np.frombuffer(raw, dtype=np.uint8)
+        rows = raw.decode("ascii").strip().splitlines()[1:]
         cols = list(zip(*[r.split(",") for r in rows]))
         num = lambda c: np.array([np.nan if v == "" else float(v) for v in c])
         out[f"{name}/iter"] = np.array([int(v) for v in cols[0]])
@@ -236,11 +238,10 @@ def demo_csv():
 
 
 if __name__ == "__main__":
-    demo_csv()
-    ve_windows()
-    operators_and_denoisers()
-    deblur_traces()
-    superres_traces()
+    sections = {"demo": demo_csv, "ve": ve_windows, "ops": operators_and_denoisers,
+                "deblur": deblur_traces, "superres": superres_traces}
+    for key in (sys.argv[1:] or list(sections)):
+        sections[key]()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
