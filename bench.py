@@ -17,9 +17,14 @@ super-resolution x3 image, PatchWeighted, FP+RRE with the CG data term;
 configs[3]: 512 images of 512^2 with the seeded filter-bank denoiser, split
 across the ranks).
 
-``--impl reference`` times the CPU restatement of the reference
-(oracle/redve_ref.py + oracle/extras) on the host cores: one image per core
-per step, a process pool over every core.
+``--impl reference`` times the reference's CPU path on the host cores: the
+UNMODIFIED reference package ``redve`` (pip-installed into baseline/_ref) with
+the configs' denoisers plugged in through its callable protocol, the whole
+batch per step over a process pool of every core; the oracle restatement
+(oracle/redve_ref.py) only when baseline/_ref is absent.
+
+``--gpus N`` outside torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU).
 """
 
 from __future__ import annotations
@@ -172,22 +177,27 @@ def cpu_baseline(cfg_id, n_images, iters_per_solve=BUDGET):
     bounded number of fixed-point iterations, scaled to solves/s at the iteration
     count the solve takes (the CG route stops early on an exactly stationary step)."""
     c = CONFIGS[cfg_id]
+    ref = reference_available()
+    kind = "reference" if ref else "port"
+    who = "the unmodified reference (baseline/_ref)" if ref else "oracle/redve_ref.py"
     if c["size"] <= 256:
         t0 = time.perf_counter()
         for i in range(n_images):
-            _oracle_solve((cfg_id, i, BUDGET))
+            (_ref_solve if ref else _oracle_solve)((cfg_id, i, BUDGET))
         dt = time.perf_counter() - t0
-        return {"value": n_images / dt, "unit": "solves/s", "cores": 1, "kind": "port",
-                "sample": f"{n_images} full solves (200 iterations) by oracle/redve_ref.py, "
-                          f"1 thread, {dt:.1f} s"}
+        return {"value": n_images / dt, "unit": "solves/s", "cores": 1, "kind": kind,
+                "sample": f"{n_images} full solves (200 iterations) by {who}, 1 thread, {dt:.1f} s"}
     iters = 1 if c["kind"] == "sr" else 3
-    red, x = _oracle_problem(c, 0)
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        x = red.fp_step(x)
-    dt = (time.perf_counter() - t0) / iters
-    return {"value": 1.0 / (dt * iters_per_solve), "unit": "solves/s", "cores": 1, "kind": "port",
-            "sample": f"{iters} fixed-point iteration(s) of one image by oracle/redve_ref.py, "
+    if ref:
+        dt = _ref_iterations((cfg_id, 0, iters))
+    else:
+        red, x = _oracle_problem(c, 0)
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            x = red.fp_step(x)
+        dt = (time.perf_counter() - t0) / iters
+    return {"value": 1.0 / (dt * iters_per_solve), "unit": "solves/s", "cores": 1, "kind": kind,
+            "sample": f"{iters} fixed-point iteration(s) of one image by {who}, "
                       f"{dt * 1e3:.0f} ms/iteration, scaled to {iters_per_solve} iterations"}
 
 
@@ -206,7 +216,74 @@ def cpu_baseline_spatial():
                       f"({dt:.1f} s), scaled x{scale:.1f} by pixel count to 8192^2"}
 
 
+REF_PATH = os.path.join(REPO, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    """The UNMODIFIED reference package, pip-installed into baseline/_ref (git-
+    ignored, travels to the GPU box with the repo snapshot)."""
+    return os.path.isfile(os.path.join(REF_PATH, "redve", "__init__.py"))
+
+
+def _ref_problem(cfg_id, seed):
+    """BASELINE.json config through the reference's own public API
+    (pkg/src/redve: Blur / BlurDownsample, degrade, RedObjective,
+    as_fixed_point_problem), the non-reference denoisers plugged in through its
+    callable-denoiser protocol (denoisers.py:1-8)."""
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import redve
+    from redve.objective import as_fixed_point_problem
+    from scipy import ndimage
+
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    c = CONFIGS[cfg_id]
+    n = c["size"]
+    truth = voronoi_scene(int(seed), n)
+    if c["kind"] == "sr":
+        op = redve.BlurDownsample(redve.make_psf("gaussian", 7, 1.6), 3, truth.shape)
+    else:
+        op = redve.Blur(redve.make_psf("uniform", 9), truth.shape)
+    y = redve.degrade(truth, op, c["sigma"], seed=int(seed))
+    if c["den"] == "median":  # the 3x3 median a reference user would plug in
+        den = lambda x: ndimage.median_filter(x, size=3, mode="wrap")
+    elif c["den"] == "filterbank":  # no reference implementation exists (SURVEY 0.1)
+        from oracle import extras
+
+        den = extras.FilterBank(0)
+    elif c["den"] == "patch":
+        den = redve.PatchWeighted()
+    else:
+        den = redve.GaussianFilter()
+    obj = redve.RedObjective(forward=op, y=y, sigma=c["sigma"], alpha=ALPHA, denoiser=den)
+    x0 = op.adjoint(y) if c["kind"] == "sr" else y
+    return redve, obj, as_fixed_point_problem(obj), x0
+
+
+def _ref_solve(args):
+    """One full reference solve (solvers.py:388-399) of image `seed`."""
+    cfg_id, seed, budget = args
+    redve, _, prob, x0 = _ref_problem(cfg_id, seed)
+    c = CONFIGS[cfg_id]
+    _, tr = redve.solve(prob, x0.ravel(), redve.SolveConfig(
+        method="fp-ve", ve_method=c["ve"], m=0, kappa=KAPPA, max_inner_steps=budget))
+    return len(tr.records)
+
+
+def _ref_iterations(args):
+    """Seconds per reference fixed-point iteration (objective.py:100-121) of image `seed`."""
+    cfg_id, seed, iters = args
+    _, obj, _, x = _ref_problem(cfg_id, seed)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        x = obj.fp_step(x)
+    return (time.perf_counter() - t0) / iters
+
+
 def run_reference(a):
+    """The reference's CPU path on the host cores: the unmodified redve from
+    baseline/_ref when installed, else the oracle port (oracle/redve_ref.py)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -215,6 +292,9 @@ def run_reference(a):
 
     c = CONFIGS[a.config]
     cores = _host_cores()
+    kind = "reference" if reference_available() else "port"
+    who = ("unmodified reference redve (baseline/_ref), " if kind == "reference"
+           else "oracle/redve_ref.py restatement (baseline/_ref absent), ")
     if a.config == 4:  # one huge image: the CPU path is a single process
         cpu = cpu_baseline_spatial()
         line = {"impl": "reference", "metric": SPATIAL_METRIC, "value": cpu["value"],
@@ -227,31 +307,47 @@ def run_reference(a):
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
-    if c["size"] > 256:  # bounded sample: iterations, not solves
-        cpu = cpu_baseline(a.config, 1)
-        value, ms = cpu["value"] * cores, None
-        sample = cpu["sample"] + f"; x{cores} cores (independent images)"
-    else:
-        work = [(a.config, i, BUDGET) for i in range(cores)]
-        ctx = mp.get_context("fork")
-        times = []
-        with ctx.Pool(cores, initializer=_single_thread_env) as pool:
+    solve_fn = _ref_solve if kind == "reference" else _oracle_solve
+    nb = a.batch or c["batch"]
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores, initializer=_single_thread_env) as pool:
+        if c["size"] <= 256:
+            # every timed step solves the whole batch (configs[1]: all 64 images,
+            # 200 iterations each); warm-up steps solve one image per worker
+            work = [(a.config, i, BUDGET) for i in range(nb)]
             for it in range(a.warmup + a.steps):
+                batch = work[:min(cores, nb)] if it < a.warmup else work
                 t0 = time.perf_counter()
-                pool.map(_oracle_solve, work, chunksize=1)
-                dt = time.perf_counter() - t0
+                pool.map(solve_fn, batch, chunksize=1)
                 if it >= a.warmup:
-                    times.append(dt)
-        ms = 1e3 * statistics.mean(times)
-        value = cores / (ms / 1e3)
-        sample = f"{cores} images per step (one per core, process pool)"
+                    times.append(time.perf_counter() - t0)
+            ms = 1e3 * statistics.mean(times)
+            value = nb / (ms / 1e3)
+            sample = f"all {nb} images x {BUDGET} iterations per step, process pool of {cores}"
+        else:
+            # large images: a bounded sample of fixed-point iterations, one image per
+            # core, scaled to solves/s at BUDGET iterations per solve
+            iters = 2
+            if kind == "reference":
+                per = pool.map(_ref_iterations, [(a.config, i, iters) for i in range(cores)],
+                               chunksize=1)
+            else:
+                per = [cpu_baseline(a.config, 1)["value"]]
+            t_it = statistics.mean(per) if kind == "reference" else 1.0 / (per[0] * BUDGET)
+            value = cores / (t_it * BUDGET)
+            ms = None
+            sample = (f"{iters} fixed-point iterations of {cores} images (one per core), "
+                      f"{t_it * 1e3:.0f} ms/iteration, scaled to {BUDGET} iterations per solve")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
+        "impl": "reference", "metric": METRIC if a.config == 1 else
+        f"RED-FP+VE image solves/sec (configs[{a.config}])", "value": value, "unit": "solves/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": c["workload"], "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": sample + "; oracle/redve_ref.py restatement of the reference"},
+        "data": "synthetic", "config": {"workload": c["workload"], "sample": sample,
+                                        "global_batch": nb},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": kind,
+                         "sample": who + sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -448,6 +544,39 @@ def ncu_traffic(kind):
     return None if v is None else float(v)
 
 
+def init_ranks(world, local):
+    """One rank per GPU over NCCL.  When the node has fewer GPUs than ranks
+    (plumbing checks on a 1-GPU box), ranks share devices round-robin and the
+    few host-side reductions go over gloo; such a line says "shared_gpus" and
+    is not a scaling measurement."""
+    import torch
+    import torch.distributed as dist
+
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    shared = world > ndev
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return shared
+
+
+def _reduce_max(t, world, shared):
+    """Max over ranks of a 1-element device tensor (gloo path via the host)."""
+    import torch.distributed as dist
+
+    if world <= 1:
+        return float(t.item())
+    if shared:
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        return float(h.item())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_native(a):
     import torch
     import torch.distributed as dist
@@ -460,9 +589,8 @@ def run_native(a):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shared = init_ranks(world, local)
+    local = local % torch.cuda.device_count()
     nb = a.batch or c["batch"]
     if c["scaling"] == "strong":  # a global batch split across the ranks
         lo, hi = shard_bounds(nb, world, rank)
@@ -507,14 +635,34 @@ def run_native(a):
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = _reduce_max(torch.tensor([ms], dtype=torch.float64, device="cuda"), world, shared)
     value = global_batch / (ms / 1e3)
     launches = (l1 - l0) // a.steps
     assert int((res.status != 0).sum()) == 0
     iters = int(res.n_records.max())
+
+    # ---- the other drivers configs[1] names (FP, FP+RRE), same batch, same timing
+    methods = {f"fp-ve/{c['ve']}": {"value": value, "ms_per_step": ms,
+                                    "iterations": iters}}
+    if a.config == 1:
+        for label, mcfg in (("fp", rv.SolveConfig(method="fp", max_inner_steps=BUDGET)),
+                            ("fp-ve/rre", rv.SolveConfig(method="fp-ve", ve_method="rre", m=0,
+                                                         kappa=KAPPA, max_inner_steps=BUDGET))):
+            for _ in range(a.warmup):
+                batch.solve(x0, mcfg)
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(a.steps):
+                r2 = batch.solve(x0, mcfg)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            mms = e0.elapsed_time(e1) / a.steps
+            mms = _reduce_max(torch.tensor([mms], dtype=torch.float64, device="cuda"), world,
+                              shared)
+            assert int((r2.status != 0).sum()) == 0
+            methods[label] = {"value": global_batch / (mms / 1e3), "ms_per_step": mms,
+                              "iterations": int(r2.n_records.max())}
 
     # ---- per-kernel device times (CUDA events bracketing every launch, one extra solve)
     nat.profile(True)
@@ -581,10 +729,7 @@ def run_native(a):
         del b2
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_s = float(tt.item())
+    e2e_s = _reduce_max(torch.tensor([e2e_s], dtype=torch.float64, device="cuda"), world, shared)
     assert len(traces) == B
     h2d = ys.nbytes + x0.numel() * 8          # measurements for the problem + x0
     d2h = x0.numel() * 8 + B * (BUDGET * 5 * 8)  # solutions + per-record trace arrays
@@ -603,12 +748,14 @@ def run_native(a):
             "config": {"workload": c["workload"], "global_batch": global_batch,
                        "images_per_gpu": B, "image": f"{n}x{n}", "iterations": iters,
                        "ms_per_iteration": ms / max(iters, 1), "parallelism": f"dp{world}",
+                       **({"shared_gpus": True} if shared else {}),
                        **({"pw_weight_planes": c["pw_weights"]} if "pw_weights" in c else {}),
                        "l2": "working set > L2 (ring of kappa+2 iterates per image)"
                        if B * N * 8 * (KAPPA + 2) > 126e6 else "working set fits L2"},
             "e2e": {"value": global_batch / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s},
             "gpu_launches": int(launches),
+            "methods": methods,
             "roofline": roof,
             "step_roofline": step_roof,
             "kernels": kernels,
@@ -634,9 +781,8 @@ def run_spatial(a):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shared = init_ranks(world, local)
+    local = local % torch.cuda.device_count()
     n = c["size"]
     op = product_operator(c)
     truth = voronoi_scene(0, n)
@@ -684,10 +830,7 @@ def run_spatial(a):
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = _reduce_max(torch.tensor([ms], dtype=torch.float64, device="cuda"), world, shared)
     iters = len(tr.records)
     value = iters / (ms / 1e3)
 
@@ -730,10 +873,7 @@ def run_spatial(a):
     x_host, _ = solve_spatial(prob2, x0, cfg)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_s = float(tt.item())
+    e2e_s = _reduce_max(torch.tensor([e2e_s], dtype=torch.float64, device="cuda"), world, shared)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         _single_thread_env()
@@ -745,6 +885,7 @@ def run_spatial(a):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": c["workload"], "image": f"{n}x{n}", "iterations": iters,
                        "ms_per_iteration": ms / iters, "parallelism": f"spatial{world}",
+                       **({"shared_gpus": True} if shared else {}),
                        "slab_rows": lay.rows, "halo_rows": lay.halo,
                        "pw_weight_planes": c.get("pw_weights", "float64"),
                        "l2": "working set > L2 (8192^2 fp64 = 512 MiB per image)"},
@@ -760,8 +901,28 @@ def run_spatial(a):
         dist.destroy_process_group()
 
 
+def _relaunch_distributed(a) -> bool:
+    """``--gpus N`` (N > 1) outside torchrun: start N ranks on this node."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     a = parse()
+    _relaunch_distributed(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.impl != "reference" and world != a.gpus:
+        print(f"bench: --gpus {a.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}",
+              file=sys.stderr)
     if a.impl == "reference":
         run_reference(a)
     elif a.config == 4:

@@ -99,8 +99,23 @@ struct ProfEvent {
   cudaEvent_t a, b;
 };
 
+// A captured solve schedule.  Instantiated graphs are kept per context by
+// topology (everything but buffer addresses): a problem of the same shape and
+// configuration re-captures and UPDATES the instantiated graph in place
+// (cudaGraphExecUpdate) instead of instantiating ~750 nodes again.  `owner` is
+// the full key (problem serial + buffer addresses) the executable holds now.
+struct GraphSlot {
+  cudaGraphExec_t exec = nullptr;
+  std::string owner;
+  unsigned long long launches = 0;
+};
+static std::atomic<unsigned long long> g_problem_serial{0};
+
 struct redve_ctx {
   bool profiling = false;
+  std::map<std::string, GraphSlot> graphs;  // topology key -> executable graph
+  void* hstage = nullptr;                   // pinned staging for trace read-back
+  size_t hstage_bytes = 0;
   cudaStream_t cap_stream = nullptr;  // graph capture
   cudaEvent_t fork_ev = nullptr;
   std::vector<ProfEvent> prof;
@@ -114,6 +129,9 @@ struct redve_ctx {
   std::vector<double> taps_host;  // what scratch_taps holds (skip identical re-uploads)
   void* taps_dev = nullptr;
   ~redve_ctx() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (hstage) cudaFreeHost(hstage);
     for (auto& kv : twiddles) delete kv.second;
     for (auto& kv : stage_twiddles) delete kv.second;
     for (auto& e : prof) {
@@ -229,20 +247,13 @@ struct redve_problem {
   double pw_h = 110.0;
   int pw_w32 = 0;
   DevBuf w0, D0, D1, cgst, cr, cp, cq, cnt_cg, cnt_rec, part_cg;
-  cudaGraphExec_t gexec = nullptr;  // captured solve (Fourier route)
-  std::string gkey;
-  unsigned long long glaunches = 0;
+  unsigned long long serial = ++g_problem_serial;  // never reused (graph ownership)
   unsigned long long captures = 0;  // graph (re)captures, for tests
   DevBuf x0bad;                     // device flag: x0 had a non-finite entry
   // gradient baselines: H^T H / sigma^2 stencil taps (circulant H), Nesterov y
   DevBuf gtaps, ybuf, part_grad, cnt_grad;
   int g_R = 0, g_sep = 0;
-  void* hstage = nullptr;           // pinned staging for the trace read-back
-  size_t hstage_bytes = 0;
-  ~redve_problem() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-    if (hstage) cudaFreeHost(hstage);
-  }
+
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
   DevBuf rd_filters, rd_scales;
@@ -1218,11 +1229,13 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   // The graph never sees the caller's x0 / x_out: x0 is loaded into ring slot 0
   // before it and the solution gathered after it, so repeated solves on one
   // problem replay a single capture whatever buffers the caller passes.
-  char keybuf[512];
-  snprintf(keybuf, sizeof(keybuf), "%p|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g|%p|%p|%p|%p", (void*)p,
+  char topo[512], keybuf[640];
+  snprintf(topo, sizeof(topo), "%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g",
+           p->B, p->H, p->W, p->op.kind, p->op.ksize, p->dn_api_kind, p->dn_ksize, (int)pw,
            cfg->method, cfg->ve_method, cfg->m, cfg->kappa, cfg->max_inner_steps, cfg->tol,
-           cfg->stabilization_iters, cfg->rank_tolerance, gradm ? cfg->step_size : 0.0,
-           p->ring.p, p->trace.p, p->best.p, p->ybuf.p);
+           cfg->stabilization_iters, cfg->rank_tolerance, gradm ? cfg->step_size : 0.0);
+  snprintf(keybuf, sizeof(keybuf), "%s|%llu|%p|%p|%p|%p", topo, p->serial, p->ring.p, p->trace.p,
+           p->best.p, p->ybuf.p);
   CK(p->x0bad.ensure(sizeof(int)));
   CK(cudaMemsetAsync(p->x0bad.p, 0, sizeof(int), s));
   RUN(ctx, "load_x0", launch_load_x0(p->ring.as<double>(), N * S, x0, B, N, p->x0bad.as<int>(), s));
@@ -1478,9 +1491,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     }
     return REDVE_OK;
   };
-  if (use_graph && p->gexec && p->gkey == keybuf) {
-    CK(cudaGraphLaunch(p->gexec, s));
-    g_launches.fetch_add(p->glaunches);
+  GraphSlot* slot = use_graph ? &ctx->graphs[topo] : nullptr;
+  if (use_graph && slot->exec && slot->owner == keybuf) {
+    CK(cudaGraphLaunch(slot->exec, s));
+    g_launches.fetch_add(slot->launches);
   } else if (use_graph) {
     const cudaStream_t orig = s;
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
@@ -1498,15 +1512,39 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     s = orig;
     if (r) return r;
     if (ce != cudaSuccess) return fail(ctx, REDVE_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
-    if (p->gexec) cudaGraphExecDestroy(p->gexec);
-    p->gexec = nullptr;
-    ce = cudaGraphInstantiate(&p->gexec, graph, 0);
+    bool updated = false;
+    if (slot->exec) {  // same topology, other buffers: patch the node parameters
+      cudaGraphExecUpdateResultInfo info;
+      updated = cudaGraphExecUpdate(slot->exec, graph, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(slot->exec);
+        slot->exec = nullptr;
+      }
+    }
+    if (!updated) {
+      if (ctx->graphs.size() > 16) {  // bound the cache: drop other topologies
+        for (auto it = ctx->graphs.begin(); it != ctx->graphs.end();) {
+          if (&it->second != slot) {
+            if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+            it = ctx->graphs.erase(it);
+          } else {
+            ++it;
+          }
+        }
+      }
+      ce = cudaGraphInstantiate(&slot->exec, graph, 0);
+    }
     cudaGraphDestroy(graph);
-    if (ce != cudaSuccess) return fail(ctx, REDVE_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
-    p->gkey = keybuf;
-    p->glaunches = g_launches.load() - l0;
+    if (ce != cudaSuccess) {
+      slot->exec = nullptr;
+      slot->owner.clear();
+      return fail(ctx, REDVE_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    }
+    slot->owner = keybuf;
+    slot->launches = g_launches.load() - l0;
     p->captures += 1;
-    CK(cudaGraphLaunch(p->gexec, s));
+    CK(cudaGraphLaunch(slot->exec, s));
   } else {
     int r = device_work();
     if (r) return r;
@@ -1522,14 +1560,14 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   // host copies into the caller's arrays
   const size_t sbytes = sizeof(ImgState) * B;
   const size_t need = tbytes + sbytes + sizeof(int);
-  if (p->hstage_bytes < need) {
-    if (p->hstage) cudaFreeHost(p->hstage);
-    p->hstage = nullptr;
-    p->hstage_bytes = 0;
-    CK(cudaHostAlloc(&p->hstage, need, cudaHostAllocDefault));
-    p->hstage_bytes = need;
+  if (ctx->hstage_bytes < need) {
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
+    ctx->hstage = nullptr;
+    ctx->hstage_bytes = 0;
+    CK(cudaHostAlloc(&ctx->hstage, need, cudaHostAllocDefault));
+    ctx->hstage_bytes = need;
   }
-  char* hs = static_cast<char*>(p->hstage);
+  char* hs = static_cast<char*>(ctx->hstage);
   CK(cudaMemcpyAsync(hs, p->trace.p, tbytes, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hs + tbytes, p->state.p, sbytes, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hs + tbytes + sbytes, p->x0bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -18,7 +18,7 @@ SQRT2 = float(np.sqrt(2.0))
 
 
 def rel(a, b):
-    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
@@ -40,8 +40,8 @@ def cmp_trace(tr, g, key, cost_rtol=1e-9):
     m = ~np.isnan(gp)
     assert np.max(np.abs(ps[m] - gp[m]), initial=0.0) <= 0.01
     sn, gs = tr.step_norms(), g[f"{key}/step_norm"]
-    m = gs > 1e-12
-    np.testing.assert_allclose(sn[m], gs[m], rtol=1e-6)
+    # below ~1e-10 a step norm is fp64 rounding noise of the iterates
+    np.testing.assert_allclose(sn, gs, rtol=1e-6, atol=1e-13)
     gam = np.array([np.nan if r.gamma_abs_sum is None else r.gamma_abs_sum for r in tr.records])
     assert np.array_equal(np.isnan(gam), np.isnan(g[f"{key}/gamma_abs_sum"]))
     assert len(tr.cycle_weights) == int(g[f"{key}/n_cycles"])
@@ -68,7 +68,11 @@ def test_g32_gradient_methods_vs_reference(rv, golden, name, cfg):
     assert prob.red.device_solvable
     x, tr = rv.solve(prob, y.ravel(), conf)
     assert rel(x, g[f"g32/{name}/x"]) <= 1e-5
-    cmp_trace(tr, g, f"g32/{name}")
+    # SD-MPE with kappa = 8: the windows' pivot ratios reach ~2e-7 (cond(R) ~ 1e7),
+    # and the reference itself moves its costs by 1.9e-5 (x by 8e-6) when its
+    # windows are perturbed by 1e-15 relative (/tmp experiment recorded in
+    # DESIGN.md section 4): costs are compared at the reference's own resolution
+    cmp_trace(tr, g, f"g32/{name}", cost_rtol=1e-4 if name == "sdmpe" else 1e-9)
 
 
 @pytest.mark.parametrize("name,run", [("sd", "run_steepest_descent"), ("nesterov", "run_nesterov")])
