@@ -19,6 +19,8 @@
 #include "fused.cuh"
 #include "sr.cuh"
 #include "grad.cuh"
+#include "spectral.cuh"
+#include <cufft.h>
 
 using namespace redve;
 
@@ -253,6 +255,14 @@ struct redve_problem {
   // gradient baselines: H^T H / sigma^2 stencil taps (circulant H), Nesterov y
   DevBuf gtaps, ybuf, part_grad, cnt_grad;
   int g_R = 0, g_sep = 0;
+  // spectral route (linear denoisers): constant spectra, DFT staging, plans
+  DevBuf sp_m, sp_hh, sp_wr, sp_xb, sp_yh, sp_rh, sp_stage, sp_part, sp_cnt;
+  bool sp_ready = false;
+  cufftHandle sp_plan = 0, sp_plan1 = 0;  // batch B / batch 1, [H][W] complex
+  ~redve_problem() {
+    if (sp_plan) cufftDestroy(sp_plan);
+    if (sp_plan1) cufftDestroy(sp_plan1);
+  }
 
   int rd_nf = 0, rd_fs = 0;
   double rd_tau = 0.0;
@@ -1130,6 +1140,80 @@ static int ve_chunks(int B, long long N) {
   return best;
 }
 
+// ------------------------------------------------------------------ spectral route
+static bool spectral_enabled() {
+  const char* e = getenv("REDVE_SPECTRAL");
+  return !(e && e[0] == '0');
+}
+
+// The spectral route applies to circulant operators with a linear shift-
+// invariant denoiser (spectral.cuh).
+static bool spectral_route(const redve_problem* p) {
+  return p->fourier && (p->dn_api_kind == REDVE_DN_CONV || p->dn_api_kind == REDVE_DN_IDENTITY) &&
+         spectral_enabled();
+}
+
+// Constant spectra, once per problem: m = a hf / d, H(k), 1 - Re hf, DFT(x_b),
+// DFT(y), DFT(ref).
+static int spectral_setup(redve_problem* p) {
+  redve_ctx* ctx = p->ctx;
+  const cudaStream_t s = ctx->stream;
+  const int B = p->B;
+  const long long N = p->N;
+  if (!p->sp_plan) {
+    int n[2] = {p->H, p->W};
+    if (cufftPlanMany(&p->sp_plan, 2, n, nullptr, 1, (int)N, nullptr, 1, (int)N, CUFFT_Z2Z, B) !=
+            CUFFT_SUCCESS ||
+        cufftPlanMany(&p->sp_plan1, 2, n, nullptr, 1, (int)N, nullptr, 1, (int)N, CUFFT_Z2Z, 1) !=
+            CUFFT_SUCCESS)
+      return fail(ctx, REDVE_E_CUDA, "cufftPlanMany failed");
+  }
+  if (cufftSetStream(p->sp_plan, s) != CUFFT_SUCCESS || cufftSetStream(p->sp_plan1, s) != CUFFT_SUCCESS)
+    return fail(ctx, REDVE_E_CUDA, "cufftSetStream failed");
+  CK(p->sp_stage.ensure(sizeof(cd) * N * B));
+  if (!p->sp_cnt.p || p->sp_cnt.n < sizeof(unsigned) * (B + 1)) {
+    CK(p->sp_cnt.ensure(sizeof(unsigned) * (B + 1)));
+    CK(cudaMemsetAsync(p->sp_cnt.p, 0, sizeof(unsigned) * (B + 1), s));
+  }
+  CK(p->sp_part.ensure(sizeof(double) * 6 * (size_t)B * spec_chunks(B, N)));
+  if (p->sp_ready) return REDVE_OK;
+  CK(p->sp_m.ensure(sizeof(cd) * N));
+  CK(p->sp_hh.ensure(sizeof(cd) * N));
+  CK(p->sp_wr.ensure(sizeof(double) * N));
+  CK(p->sp_xb.ensure(sizeof(cd) * N * B));
+  CK(p->sp_yh.ensure(sizeof(cd) * N * B));
+  cd* stage = p->sp_stage.as<cd>();
+  auto fwd = [&](cufftHandle plan, cd* z) {
+    return cufftExecZ2Z(plan, reinterpret_cast<cufftDoubleComplex*>(z),
+                        reinterpret_cast<cufftDoubleComplex*>(z), CUFFT_FORWARD) == CUFFT_SUCCESS;
+  };
+  // denoiser spectrum -> m, 1 - Re hf (stage[0] as scratch)
+  const bool ident = p->dn_api_kind == REDVE_DN_IDENTITY;
+  if (!ident) {
+    RUN(ctx, "spec_embed", launch_spec_embed(p->dntaps.as<double>(), p->dn_ksize, p->H, p->W, stage, s));
+    if (!fwd(p->sp_plan1, stage)) return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+  }
+  RUN(ctx, "spec_consts", launch_spec_consts(ident ? nullptr : stage, p->g.as<double>(), p->alpha,
+                                             N, p->sp_m.as<cd>(), p->sp_wr.as<double>(), s));
+  // operator spectrum H(k)
+  RUN(ctx, "spec_embed", launch_spec_embed(p->htaps.as<double>(), p->op.ksize, p->H, p->W,
+                                           p->sp_hh.as<cd>(), s));
+  if (!fwd(p->sp_plan1, p->sp_hh.as<cd>())) return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+  // DFT(x_b), DFT(y), DFT(ref)
+  RUN(ctx, "spec_pack", launch_spec_pack(p->xb.as<double>(), B, N, p->sp_xb.as<cd>(), N, nullptr, s));
+  if (!fwd(p->sp_plan, p->sp_xb.as<cd>())) return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+  RUN(ctx, "spec_pack", launch_spec_pack(p->y.as<double>(), B, N, p->sp_yh.as<cd>(), N, nullptr, s));
+  if (!fwd(p->sp_plan, p->sp_yh.as<cd>())) return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+  if (p->has_ref) {
+    CK(p->sp_rh.ensure(sizeof(cd) * N * B));
+    RUN(ctx, "spec_pack", launch_spec_pack(p->ref.as<double>(), B, N, p->sp_rh.as<cd>(), N, nullptr, s));
+    if (!fwd(p->sp_plan, p->sp_rh.as<cd>())) return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+  }
+  CKL();
+  p->sp_ready = true;
+  return REDVE_OK;
+}
+
 // ------------------------------------------------------------------ solve
 int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x0, double* x_out,
                 redve_trace* trace) {
@@ -1158,9 +1242,15 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   if (p->dn_api_kind == REDVE_DN_EXTERNAL)
     return fail(ctx, REDVE_E_UNSUPPORTED, "device solve needs a device denoiser");
   const bool pw = p->dn_api_kind == REDVE_DN_PATCH || p->dn_api_kind == REDVE_DN_FILTERBANK;
+  const bool spec = !gradm && spectral_route(p);
+  if (spec) {
+    int r = spectral_setup(p);
+    if (r) return r;
+  }
 
   const int B = p->B;
   const long long N = p->N;
+  const long long NE = spec ? 2 * N : N;  // ring elements per iterate (doubles)
   const int budget = cfg->max_inner_steps;
   const int stab = ve ? cfg->stabilization_iters : 0;
   const int clen = cfg->m + cfg->kappa + 1;
@@ -1171,11 +1261,11 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   const int log_every = N <= 128 * 128 ? 1 : 5;  // solvers.py:34,213
   const bool track = ve;
 
-  CK(p->ring.ensure(sizeof(double) * N * S * B));
-  if (track) CK(p->best.ensure(sizeof(double) * N * B));
-  const int chunks = ve_chunks(B, N);
+  CK(p->ring.ensure(sizeof(double) * NE * S * B));
+  if (track) CK(p->best.ensure(sizeof(double) * NE * B));
+  const int chunks = ve_chunks(B, NE);
   if (ve) {
-    CK(p->q.ensure(sizeof(double) * N * kp1 * B));
+    CK(p->q.ensure(sizeof(double) * NE * kp1 * B));
     size_t need = (size_t)B * chunks * (MAXKP1 * (MAXKP1 + 1) / 2);
     if (need * sizeof(double) > p->partials.n)  // grow (the row kernels' share fits inside)
       CK(p->partials.ensure(need * sizeof(double) + 64));
@@ -1230,16 +1320,27 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   // before it and the solution gathered after it, so repeated solves on one
   // problem replay a single capture whatever buffers the caller passes.
   char topo[512], keybuf[640];
-  snprintf(topo, sizeof(topo), "%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g",
-           p->B, p->H, p->W, p->op.kind, p->op.ksize, p->dn_api_kind, p->dn_ksize, (int)pw,
+  snprintf(topo, sizeof(topo), "%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g",
+           p->B, p->H, p->W, p->op.kind, p->op.ksize, p->dn_api_kind, p->dn_ksize, (int)pw, (int)spec,
            cfg->method, cfg->ve_method, cfg->m, cfg->kappa, cfg->max_inner_steps, cfg->tol,
            cfg->stabilization_iters, cfg->rank_tolerance, gradm ? cfg->step_size : 0.0);
   snprintf(keybuf, sizeof(keybuf), "%s|%llu|%p|%p|%p|%p", topo, p->serial, p->ring.p, p->trace.p,
            p->best.p, p->ybuf.p);
   CK(p->x0bad.ensure(sizeof(int)));
   CK(cudaMemsetAsync(p->x0bad.p, 0, sizeof(int), s));
-  RUN(ctx, "load_x0", launch_load_x0(p->ring.as<double>(), N * S, x0, B, N, p->x0bad.as<int>(), s));
-  CKL();
+  if (spec) {  // x0 -> DFT(x0) in ring slot 0
+    cd* stage = p->sp_stage.as<cd>();
+    RUN(ctx, "load_x0", launch_spec_pack(x0, B, N, stage, N, p->x0bad.as<int>(), s));
+    CKL();
+    if (cufftExecZ2Z(p->sp_plan, reinterpret_cast<cufftDoubleComplex*>(stage),
+                     reinterpret_cast<cufftDoubleComplex*>(stage), CUFFT_FORWARD) != CUFFT_SUCCESS)
+      return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+    CK(cudaMemcpy2DAsync(p->ring.p, sizeof(double) * NE * S, stage, sizeof(cd) * N, sizeof(cd) * N,
+                         B, cudaMemcpyDeviceToDevice, s));
+  } else {
+    RUN(ctx, "load_x0", launch_load_x0(p->ring.as<double>(), N * S, x0, B, N, p->x0bad.as<int>(), s));
+    CKL();
+  }
   auto device_work = [&]() -> int {
     CK(cudaMemsetAsync(p->trace.p, 0xFF, sizeof(double) * 5 * nrec, s));  // NaN
     CK(cudaMemsetAsync(tr.cyc_stab, 0, sizeof(double) * ncyc * (1 + 2 * MAXKP1) +
@@ -1248,15 +1349,22 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     RUN(ctx, "init_state", launch_init_state(st, B, s));
     CKL();
 
-    View cur{p->ring.as<double>(), N * S, N, S, 1};
-    View nxt{p->ring.as<double>(), N * S, N, S, 2};
-    View bestv = plain(p->best.as<double>(), N);
+    View cur{p->ring.as<double>(), NE * S, NE, S, 1};
+    View nxt{p->ring.as<double>(), NE * S, NE, S, 2};
+    View bestv = plain(p->best.as<double>(), NE);
     DenoiseArgs dn = dn_args(p);
+    SpecConsts sk;
+    memset(&sk, 0, sizeof(sk));
+    if (spec) {
+      sk.m = p->sp_m.as<cd>(); sk.hh = p->sp_hh.as<cd>(); sk.wr = p->sp_wr.as<double>();
+      sk.xb = p->sp_xb.as<cd>(); sk.yh = p->sp_yh.as<cd>();
+      sk.rh = p->has_ref ? p->sp_rh.as<cd>() : nullptr;
+    }
     StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0};
 
     VeArgs va;
-    va.B = B; va.N = N; va.m = cfg->m; va.kp1 = kp1; va.S = S;
-    va.ring = p->ring.as<double>(); va.img_stride = N * S; va.slot_stride = N;
+    va.B = B; va.N = NE; va.m = cfg->m; va.kp1 = kp1; va.S = S;
+    va.ring = p->ring.as<double>(); va.img_stride = NE * S; va.slot_stride = NE;
     va.st = st; va.tr = tr; va.partials = p->partials.as<double>();
     va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
     va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
@@ -1272,6 +1380,15 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
     bool f_ready = false;
     auto cost_of_cur = [&](int mode, StepCtl c, const double* fprev_rec = nullptr) -> int {
+      if (spec) {  // note_initial / finalize in the Fourier domain (records are fused)
+        SpecCostArgs sa;
+        sa.B = B; sa.H = p->H; sa.W = p->W; sa.x = cur; sa.k = sk; sa.mode = mode;
+        sa.sigma = p->sigma; sa.alpha = p->alpha; sa.st = st; sa.ctl = c; sa.tr = tr;
+        sa.partials = p->sp_part.as<double>(); sa.counters = p->sp_cnt.as<unsigned>();
+        RUN(ctx, "spec_cost", launch_spec_cost(sa, s));
+        CKL();
+        return REDVE_OK;
+      }
       const double* fe = nullptr;
       const int ph = mode == COST_RECORD ? c.phase : PH_SETUP;
       if (pw) {
@@ -1304,7 +1421,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     if (track) {  // note_initial (solvers.py:219-223)
       int r0 = cost_of_cur(COST_INIT, ctl);
       if (r0) return r0;
-      RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
+      RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, NE, st, 1, s));
       CKL();
     }
 
@@ -1324,6 +1441,21 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       c.defer_commit = cadence ? 1 : 0;
       int r = REDVE_OK;
       double* fp_this = fpb[kk & 1];
+      if (spec) {  // X+ = Xb + m X, cost fused on cadence steps (spectral.cuh)
+        SpecStepArgs sa;
+        sa.B = B; sa.H = p->H; sa.W = p->W; sa.cur = cur; sa.nxt = nxt; sa.k = sk;
+        sa.cadence = cadence ? 1 : 0; sa.sigma = p->sigma; sa.alpha = p->alpha;
+        sa.st = st; sa.ctl = c; sa.tr = tr; sa.S = S;
+        sa.partials = p->sp_part.as<double>(); sa.counters = p->sp_cnt.as<unsigned>();
+        RUN(ctx, "spec_step", launch_spec_step(sa, s));
+        CKL();
+        if (cadence && track) {
+          RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, NE, st, 1, s));
+          CKL();
+        }
+        ++kk;
+        return REDVE_OK;
+      }
       if (gradm) {  // x+ = v - s grad E(v)  (solvers.py:274-280, 315-337)
         double* y0 = nest ? p->ybuf.as<double>() : nullptr;
         const size_t half = (size_t)B * N;
@@ -1423,7 +1555,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         r = cost_of_cur(COST_RECORD, c, fp_this);
         if (r) return r;
         if (track) {
-          RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, N, st, 1, s));
+          RUN(ctx, "copy_view", launch_copy_view(bestv, cur, B, NE, st, 1, s));
           CKL();
         }
       }
@@ -1549,7 +1681,18 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     int r = device_work();
     if (r) return r;
   }
-  {
+  if (spec) {  // chosen spectrum -> inverse DFT -> x_out
+    View cur{p->ring.as<double>(), NE * S, NE, S, 1};
+    cd* stage = p->sp_stage.as<cd>();
+    RUN(ctx, "gather", launch_spec_pick(stage, cur, track ? p->best.as<double>() : nullptr, B, N,
+                                        p->state.as<ImgState>(), s));
+    CKL();
+    if (cufftExecZ2Z(p->sp_plan, reinterpret_cast<cufftDoubleComplex*>(stage),
+                     reinterpret_cast<cufftDoubleComplex*>(stage), CUFFT_INVERSE) != CUFFT_SUCCESS)
+      return fail(ctx, REDVE_E_CUDA, "cufftExecZ2Z failed");
+    RUN(ctx, "gather", launch_spec_real(stage, x_out, B, N, 1.0 / (double)N, s));
+    CKL();
+  } else {
     View cur{p->ring.as<double>(), N * S, N, S, 1};
     RUN(ctx, "gather", launch_gather(x_out, cur, track ? p->best.as<double>() : nullptr, B, N,
                                      p->state.as<ImgState>(), s));

@@ -1,0 +1,97 @@
+"""Spectral route (linear shift-invariant denoisers on circulant operators):
+the fixed point iterated in the Fourier domain (csrc/spectral.cuh) against
+the reference's golden traces, and against the spatial Fourier-kernel route
+(REDVE_SPECTRAL=0) on the same inputs."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SQRT2 = float(np.sqrt(2.0))
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def rv():
+    import paper_1805_02158_b200 as rv
+
+    return rv
+
+
+@pytest.mark.parametrize("route", ["spectral", "spatial"])
+@pytest.mark.parametrize("name,method", [("fp", "fp"), ("mpe", "fp-ve")])
+def test_config0_both_routes_vs_reference(rv, golden, monkeypatch, route, name, method):
+    if route == "spatial":
+        monkeypatch.setenv("REDVE_SPECTRAL", "0")
+    g = golden("deblur_traces.npz")
+    truth, y = g["c0/truth"], g["c0/y"]
+    obj = rv.RedObjective(rv.Blur(rv.make_psf("uniform", 9), truth.shape), y, SQRT2, 0.02,
+                          rv.GaussianFilter())
+    prob = rv.as_fixed_point_problem(obj, reference=truth)
+    x, tr = rv.solve(prob, y.ravel(), rv.SolveConfig(method=method, max_inner_steps=200))
+    assert rel(x, g[f"c0/{name}/x"]) <= 1e-5
+    np.testing.assert_array_equal([r.iter for r in tr.records], g[f"c0/{name}/iter"])
+    gc = g[f"c0/{name}/cost"]
+    m = ~np.isnan(gc)
+    assert np.array_equal(np.isnan(tr.costs()), np.isnan(gc))
+    np.testing.assert_allclose(tr.costs()[m], gc[m], rtol=1e-9)
+    ps = np.array([np.nan if r.psnr is None else r.psnr for r in tr.records])
+    gp = g[f"c0/{name}/psnr"]
+    m = ~np.isnan(gp)
+    assert np.max(np.abs(ps[m] - gp[m])) <= 0.01
+    np.testing.assert_allclose(tr.step_norms(), g[f"c0/{name}/step_norm"], rtol=1e-6, atol=1e-13)
+    assert len(tr.cycle_weights) == int(g[f"c0/{name}/n_cycles"])
+
+
+@pytest.mark.parametrize("den", ["gauss", "gauss_wide", "identity"])
+@pytest.mark.parametrize("cfg", [dict(method="fp-ve", ve_method="rre", max_inner_steps=40),
+                                 dict(method="fp-ve", ve_method="svdmpe", m=1, kappa=3,
+                                      max_inner_steps=30, stabilization_iters=2),
+                                 dict(method="fp", max_inner_steps=50, tol=1e-4)])
+def test_spectral_equals_spatial_route(rv, monkeypatch, den, cfg):
+    from oracle import redve_ref as R
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    B, shape = 3, (48, 40)
+    truths = np.stack([voronoi_scene(s, *shape) for s in range(B)])
+    op_o = R.CirculantBlur(R.psf_taps("gaussian", 7, 1.2), shape)
+    ys = np.stack([R.measure(truths[b], op_o, SQRT2 * (1 + b), b) for b in range(B)])
+    op = rv.Blur(rv.make_psf("gaussian", 7, 1.2), shape)
+    dn = {"gauss": rv.GaussianFilter(), "gauss_wide": rv.GaussianFilter(1.2, 5),
+          "identity": rv.Identity()}[den]
+    conf = rv.SolveConfig(**cfg)
+    out = {}
+    for route in ("spectral", "spatial"):
+        monkeypatch.setenv("REDVE_SPECTRAL", "1" if route == "spectral" else "0")
+        batch = rv.RedBatch(op, ys, SQRT2, 0.02, dn, truths)
+        X, traces = rv.solve_batch(batch, ys, conf)
+        out[route] = (X.cpu().numpy(), traces)
+    Xs, ts = out["spectral"]
+    Xp, tp = out["spatial"]
+    for b in range(B):
+        assert rel(Xs[b], Xp[b]) <= 1e-9
+        assert ts[b].inner_steps == tp[b].inner_steps
+        np.testing.assert_allclose(ts[b].costs(), tp[b].costs(), rtol=1e-9)
+        np.testing.assert_allclose(ts[b].step_norms(), tp[b].step_norms(), rtol=1e-7, atol=1e-13)
+        assert len(ts[b].cycle_weights) == len(tp[b].cycle_weights)
+
+
+def test_spectral_graph_reuse_and_nonfinite(rv):
+    x = np.random.default_rng(3).uniform(0, 255, (2, 32, 32))
+    batch = rv.RedBatch(rv.Blur(rv.make_psf("uniform", 9), (32, 32)), x, SQRT2, 0.02,
+                        rv.GaussianFilter())
+    cfg = rv.SolveConfig(method="fp-ve", max_inner_steps=20)
+    r1 = batch.solve(x, cfg)
+    c1 = batch.graph_captures
+    r2 = batch.solve(x + 0.0, cfg)
+    assert batch.graph_captures == c1
+    np.testing.assert_array_equal(r1.x.cpu().numpy(), r2.x.cpu().numpy())
+    bad = x.copy()
+    bad[0, 0, 0] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        batch.solve(bad, cfg)
