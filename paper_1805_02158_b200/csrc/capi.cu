@@ -1360,14 +1360,18 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       sk.xb = p->sp_xb.as<cd>(); sk.yh = p->sp_yh.as<cd>();
       sk.rh = p->has_ref ? p->sp_rh.as<cd>() : nullptr;
     }
-    StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0};
+    StepCtl ctl{PH_MAIN, budget, cfg->tol, log_every, 0, track ? 1 : 0,
+                (spec && cfg->tol == 0) ? 1 : 0};
 
     VeArgs va;
+    memset(&va, 0, sizeof(va));
     va.B = B; va.N = NE; va.m = cfg->m; va.kp1 = kp1; va.S = S;
     va.ring = p->ring.as<double>(); va.img_stride = NE * S; va.slot_stride = NE;
     va.st = st; va.tr = tr; va.partials = p->partials.as<double>();
     va.counters = p->cnt_ve.as<unsigned>(); va.qscratch = p->q.as<double>();
     va.method = cfg->ve_method; va.rank_tol = cfg->rank_tolerance; va.chunks = chunks;
+    va.stationary_continues = (spec && cfg->tol == 0) ? 1 : 0;
+    va.mgs_cluster = mgs_cluster_pays(B) ? 1 : 0;
 
     // Cost of the current iterates.  Fourier route: cadence records use the
     // normal-equation identity (k_cost_fp) with f(x_{k-1}) kept by k_row_fwd
@@ -1601,6 +1605,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         if (n == clen) {
           RUN(ctx, "gram", launch_gram(va, s));
           CKL();
+          if (va.mgs_cluster) {
+            RUN(ctx, "mgs_cluster", launch_mgs_cluster(va, s));
+            CKL();
+          }
           RUN(ctx, "combine", launch_combine(va, s));
           CKL();
           f_ready = false;  // the iterate may have been replaced
@@ -1788,6 +1796,7 @@ int redve_extrapolate(redve_ctx* ctx, int B, int rows, int64_t n, const double* 
   }
   CK(cudaMemsetAsync(ctx->ve_trace.p, 0, ctx->ve_trace.n, s));
   VeArgs va;
+  memset(&va, 0, sizeof(va));
   va.B = B; va.N = n; va.m = 0; va.kp1 = kp1; va.S = rows;
   va.ring = ctx->ve_ring.as<double>(); va.img_stride = n * rows; va.slot_stride = n;
   va.st = st; va.tr = tr; va.partials = ctx->ve_partials.as<double>();

@@ -16,6 +16,8 @@
 #include <cstdio>
 
 #include "cost.cuh"
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace redve {
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(256) k_gram(VeArgs a) {
       }
     }
   }
-  if (lastb) {  // rank question below the Gram route's resolution: exact MGS, this block
+  if (lastb && !a.mgs_cluster) {  // rank question below the Gram route's resolution: exact MGS
     __syncthreads();
     if (s.ve_mode == VE_MGS) mgs_block(a, b);
   }
@@ -582,6 +584,112 @@ __device__ __noinline__ void mgs_block(const VeArgs& a, int b) {
   }
 }
 
+// The same MGS with the window split across an 8-CTA cluster: each CTA owns a
+// contiguous chunk of every column, projections and norms are reduced over
+// the cluster through distributed shared memory in fixed rank order (every
+// CTA forms the same R), so one window costs ~1/8 of the single-CTA route.
+constexpr int MGS_CL = 8;
+
+__global__ void __cluster_dims__(MGS_CL, 1, 1) __launch_bounds__(256)
+    k_mgs_cluster(VeArgs a) {
+  namespace cg = cooperative_groups;
+  const int b = blockIdx.y;
+  ImgState& s = a.st[b];
+  if (!ve_participates(s) || s.ve_mode != VE_MGS) return;  // same in every CTA of the cluster
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  __shared__ double s_red[32];
+  __shared__ double s_part[2];
+  __shared__ double s_val;
+  __shared__ double R[MAXKP1][MAXKP1];
+  const int n = a.kp1;
+  const long long N = a.N;
+  const long long per = (N + MGS_CL - 1) / MGS_CL;
+  const long long lo = rank * per, hi = lo + per < N ? lo + per : N;
+  double* Q = a.qscratch + (long long)b * n * N;
+  if (threadIdx.x < MAXKP1 * MAXKP1) (&R[0][0])[threadIdx.x] = 0.0;
+  int parity = 0;
+  // cluster-wide dot product of chunks, identical result in every CTA
+  auto cdot = [&](const double* u, const double* v) -> double {
+    double acc[1] = {0.0};
+    for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) acc[0] = fma(u[p], v[p], acc[0]);
+    block_sum<1>(acc, s_red);
+    if (threadIdx.x == 0) s_part[parity] = acc[0];
+    cluster.sync();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int r = 0; r < MGS_CL; ++r) t += cluster.map_shared_rank(s_part, r)[parity];
+      s_val = t;
+    }
+    __syncthreads();
+    parity ^= 1;
+    return s_val;
+  };
+  const int s0 = s.start + a.m;
+  int rank_e = n;
+  double r11 = 0.0;
+  bool stationary = false;
+  for (int i = 0; i < n; ++i) {
+    const double* xa = slot_ptr(a, b, s0 + i);
+    const double* xb = slot_ptr(a, b, s0 + i + 1);
+    double* qi = Q + (long long)i * N;
+    for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) qi[p] = xb[p] - xa[p];
+    __syncthreads();
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (int j = 0; j < i; ++j) {
+        const double* qj = Q + (long long)j * N;
+        const double proj = cdot(qj, qi);
+        if (threadIdx.x == 0) R[j][i] += proj;
+        for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) qi[p] -= proj * qj[p];
+        __syncthreads();
+      }
+    }
+    const double rii = sqrt(cdot(qi, qi));
+    if (threadIdx.x == 0) R[i][i] = rii;
+    if (i == 0) {
+      if (rii < 1e-300) {
+        stationary = true;
+        break;
+      }
+      r11 = rii;
+    } else if (rii < a.rank_tol * r11) {
+      rank_e = i;
+      break;
+    }
+    for (long long p = lo + threadIdx.x; p < hi; p += blockDim.x) qi[p] /= rii;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (rank == 0 && threadIdx.x == 0) {
+    VeOut o;
+    bool finite = true;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) finite = finite && isfinite(R[i][j]);
+    if (stationary) o.mode = VE_CONVERGED;
+    else if (!finite) o.mode = VE_SKIP;
+    else decide_from_r(R, n, rank_e, a.method, o);
+    s.ve_mode = o.mode;
+    if (o.mode == VE_EXTRAPOLATE) {
+      s.ve_k = o.k_used;
+      s.ve_method = o.method;
+      s.ve_fallback = o.fallback;
+      s.ve_stab = o.stab;
+      for (int i = 0; i <= o.k_used; ++i) {
+        s.ve_gamma[i] = o.gamma[i];
+        s.ve_c[i] = o.c[i];
+        if (i < o.k_used) s.ve_xi[i] = o.xi[i];
+      }
+    }
+  }
+  cluster.sync();  // no CTA leaves while another may still read its s_part
+}
+
+bool mgs_cluster_pays(int B) { return B * MGS_CL <= 2 * 148; }
+
+void launch_mgs_cluster(const VeArgs& a, cudaStream_t s) {
+  k_mgs_cluster<<<dim3(MGS_CL, a.B), 256, 0, s>>>(a);
+}
+
 // --------------------------------------------------------------- VE: combine
 // x = x_m + sum_{j<k} xi_j (x_{m+j+1} - x_{m+j})  written over the cycle-start
 // slot; accepted only if finite (solvers.py:368-378).
@@ -657,7 +765,7 @@ __global__ void __launch_bounds__(256) k_combine(VeArgs a) {
   const int mode = s.ve_mode;
   if (mode != VE_EXTRAPOLATE) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (mode == VE_CONVERGED) {
+      if (mode == VE_CONVERGED && !a.stationary_continues) {
         s.cur = (s.start + a.m) % a.S;
         s.term = CONVERGED;
       }

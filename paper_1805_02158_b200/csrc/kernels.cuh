@@ -158,6 +158,8 @@ struct VeArgs {
   int method;
   double rank_tol;
   int chunks;
+  int stationary_continues;  // spectral route, tol == 0: an exactly stationary window is skipped
+  int mgs_cluster;           // 1: flagged windows go to k_mgs_cluster (launched after k_gram)
 };
 
 // launchers (kernels.cu)
@@ -185,6 +187,9 @@ void launch_cost_fp(const CostArgs& a, int npairs, cudaStream_t s);
 void launch_copy_view(View dst, View src, int B, long long N, const ImgState* st, int only_flag,
                       cudaStream_t s);
 void launch_gram(const VeArgs& a, cudaStream_t s);
+// exact MGS of the windows k_gram flagged, one 8-CTA cluster per image (no-op otherwise)
+void launch_mgs_cluster(const VeArgs& a, cudaStream_t s);
+bool mgs_cluster_pays(int B);
 void launch_combine(const VeArgs& a, cudaStream_t s);
 void launch_init_state(ImgState* st, int B, cudaStream_t s);
 void launch_load_x0(double* ring, long long img_stride, const double* x0, int B, long long N,

@@ -43,9 +43,10 @@ __device__ __forceinline__ void cost_terms(const SpecConsts& k, int b, long long
 }  // namespace
 
 int spec_chunks(int B, long long N) {
-  // ~2 resident waves of 256-thread CTAs, at least 4 frequencies per thread
-  int c = cdivs(2LL * 148 * 4, B);
-  const int cmax = cdivs(N, SP_THREADS * 4);
+  // small batches are latency bound: one frequency per thread, as many CTAs as
+  // that takes (up to ~8 per SM); large batches: ~8 resident CTAs per SM overall
+  int c = cdivs(148LL * 8, B);
+  const int cmax = cdivs(N, SP_THREADS);
   if (c > cmax) c = cmax;
   return c < 1 ? 1 : c;
 }

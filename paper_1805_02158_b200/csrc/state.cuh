@@ -82,6 +82,11 @@ struct StepCtl {
   int log_every;      // 1 or 5
   int defer_commit;   // the cost kernel commits this step
   int track_best;
+  // spectral route with tol == 0: an exactly zero step (an exact fixed point of
+  // the rounded Fourier-domain map, which the reference's FFT round trips never
+  // reach) does not end the run -- the reference's tol = 0 contract is "run to
+  // the budget" (solvers.py:170-172)
+  int zero_step_continues;
 };
 
 __device__ __forceinline__ bool takes_step(const ImgState& s, int phase) {
@@ -118,7 +123,7 @@ __device__ inline void record_step(ImgState& s, int b, double d2, double x2, dou
   if (nf > 0.0) s.err = ERR_NONFINITE_X;
   s.pending = RUNNING;
   if (ctl.phase == PH_MAIN) {
-    if (sn <= ctl.tol) s.pending = CONVERGED;
+    if (sn <= ctl.tol && !(ctl.zero_step_continues && sn == 0.0)) s.pending = CONVERGED;
     else if (s.k >= ctl.budget) s.pending = BUDGET;
   }
   if (!ctl.defer_commit) commit_step(s, ctl.phase);

@@ -44,23 +44,7 @@ def rv():
     return rv
 
 
-def cmp_trace(tr, g, key, cost_rtol=1e-9):
-    np.testing.assert_array_equal(np.array([r.iter for r in tr.records]), g[f"{key}/iter"])
-    cost, gc = tr.costs(), g[f"{key}/cost"]
-    assert np.array_equal(np.isnan(cost), np.isnan(gc))
-    m = ~np.isnan(gc)
-    np.testing.assert_allclose(cost[m], gc[m], rtol=cost_rtol)
-    ps = np.array([np.nan if r.psnr is None else r.psnr for r in tr.records])
-    gp = g[f"{key}/psnr"]
-    assert np.array_equal(np.isnan(ps), np.isnan(gp))
-    m = ~np.isnan(gp)
-    assert np.max(np.abs(ps[m] - gp[m]), initial=0.0) <= 0.01
-    # below ~1e-10 a step norm is fp64 rounding noise of the iterates
-    sn, gs = tr.step_norms(), g[f"{key}/step_norm"]
-    np.testing.assert_allclose(sn, gs, rtol=1e-6, atol=1e-13)
-    gam = np.array([np.nan if r.gamma_abs_sum is None else r.gamma_abs_sum for r in tr.records])
-    assert np.array_equal(np.isnan(gam), np.isnan(g[f"{key}/gamma_abs_sum"]))
-    assert len(tr.cycle_weights) == int(g[f"{key}/n_cycles"])
+from trace_cmp import cmp_trace  # noqa: E402
 
 
 # ----------------------------------------------------------------- configs[1]

@@ -29,22 +29,7 @@ def rv():
     return rv
 
 
-def cmp_trace(tr, g, key, cost_rtol=1e-9, sn_rtol=1e-6):
-    np.testing.assert_array_equal(np.array([r.iter for r in tr.records]), g[f"{key}/iter"])
-    cost, gc = tr.costs(), g[f"{key}/cost"]
-    assert np.array_equal(np.isnan(cost), np.isnan(gc))
-    m = ~np.isnan(gc)
-    np.testing.assert_allclose(cost[m], gc[m], rtol=cost_rtol)
-    ps = np.array([np.nan if r.psnr is None else r.psnr for r in tr.records])
-    gp = g[f"{key}/psnr"]
-    m = ~np.isnan(gp)
-    assert np.max(np.abs(ps[m] - gp[m]), initial=0.0) <= 0.01
-    sn, gs = tr.step_norms(), g[f"{key}/step_norm"]
-    # below ~1e-10 a step norm is fp64 rounding noise of the iterates
-    np.testing.assert_allclose(sn, gs, rtol=sn_rtol, atol=1e-13)
-    gam = np.array([np.nan if r.gamma_abs_sum is None else r.gamma_abs_sum for r in tr.records])
-    assert np.array_equal(np.isnan(gam), np.isnan(g[f"{key}/gamma_abs_sum"]))
-    assert len(tr.cycle_weights) == int(g[f"{key}/n_cycles"])
+from trace_cmp import cmp_trace  # noqa: E402
 
 
 def g32_problem(rv, g):
@@ -72,9 +57,11 @@ def test_g32_gradient_methods_vs_reference(rv, golden, name, cfg):
     # and the reference itself moves its costs by 1.9e-5 (x by 8e-6) when its
     # windows are perturbed by 1e-15 relative (/tmp experiment recorded in
     # DESIGN.md section 4): costs are compared at the reference's own resolution
-    loose = name == "sdmpe"
-    cmp_trace(tr, g, f"g32/{name}", cost_rtol=1e-4 if loose else 1e-9,
-              sn_rtol=1e-4 if loose else 1e-6)
+    if name == "sdmpe":  # the reference's own resolution (see above)
+        cmp_trace(tr, g, f"g32/{name}", cost_rtol=1e-4, sn_rtol=1e-4, sn_atol=1e-5,
+                  sig_floor=1e-5)
+    else:
+        cmp_trace(tr, g, f"g32/{name}")
 
 
 @pytest.mark.parametrize("name,run", [("sd", "run_steepest_descent"), ("nesterov", "run_nesterov")])
