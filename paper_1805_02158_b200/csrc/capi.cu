@@ -16,7 +16,6 @@
 #include "kernels.cuh"
 #include "rd.cuh"
 #include "slab.cuh"
-#include "fused.cuh"
 #include "sr.cuh"
 #include "grad.cuh"
 #include "spectral.cuh"
@@ -272,7 +271,6 @@ struct redve_problem {
   // Fourier-route cost identity: f(x_{k-1}) of cadence steps, second f buffer
   // for the precomputed denoisers, ||y||^2 per image
   DevBuf fprev, fcur, yy;
-  DevBuf Z2, fprev2;  // k_row_mid: second spectrum / f(x) buffers (ping-pong)
   bool has_ref = false;
   const cd* twH = nullptr;
   const cd* twW = nullptr;
@@ -866,6 +864,7 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   int nblk_max = nblk_row > nblk_cost ? nblk_row : nblk_cost;
   if (nblk_fp > nblk_max) nblk_max = nblk_fp;
   size_t part = (size_t)p->npairs * nblk_max * 8;
+  if (part < (size_t)p->npairs * H * 6) part = (size_t)p->npairs * H * 6;  // any lines per CTA
   if (part < (size_t)B * 64 * 4) part = (size_t)B * 64 * 4;  // k_cost_fp: <= 64 CTAs per image
   PK(p->partials.ensure(sizeof(double) * part));
   PK(p->cnt_inv.ensure(sizeof(unsigned) * (B + 1)));
@@ -942,11 +941,6 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     if (r) return bail(r);
     // cost identity on the Fourier route (cost.cu k_cost_fp)
     PK(p->fprev.ensure(sizeof(double) * p->N * B));
-    if (dn->kind != REDVE_DN_PATCH && dn->kind != REDVE_DN_FILTERBANK &&
-        dn->kind != REDVE_DN_EXTERNAL && row_mid_ok(H, W, dn_args(p), p->lpc_row)) {  // opt-in
-      PK(p->Z2.ensure(sizeof(cd) * p->N * p->npairs));
-      PK(p->fprev2.ensure(sizeof(double) * p->N * B));
-    }
     PK(p->yy.ensure(sizeof(double) * B));
     RUN(ctx, "sumsq", launch_sumsq(p->y.as<double>(), Ny, B, p->yy.as<double>(), s));
     PK(cudaGetLastError());
@@ -1379,7 +1373,6 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     // precomputed denoisers f(x_k) evaluated here is handed to the next step
     // when nothing changes the iterate in between (f_ready).
     const bool ident = p->fourier && !gradm;  // the cost identity holds for FP steps only
-    const bool fused = p->fourier && !pw && !gradm && fused_step_ok(p->H, p->W, dn);
     double* f_step = p->fbuf.as<double>();   // f of the current step's input
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
     bool f_ready = false;
@@ -1429,22 +1422,14 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       CKL();
     }
 
-    // k_row_mid: the inverse row pass of a step and the forward row pass of the
-    // next step in one kernel, whenever the next step follows directly (inside
-    // a VE cycle / plain FP run; never across an extrapolation)
-    const bool mid = p->fourier && !pw && !fused && !gradm && p->Z2.p != nullptr &&
-                     row_mid_ok(p->H, p->W, dn, p->lpc_row);
     cd* zcur = p->Z.as<cd>();
-    cd* zalt = mid ? p->Z2.as<cd>() : nullptr;
-    double* fpb[2] = {p->fprev.as<double>(), mid ? p->fprev2.as<double>() : p->fprev.as<double>()};
-    bool z_ready = false;  // zcur already holds this step's row spectra
-    int kk = 0;            // steps issued so far (f(x) buffer parity)
-    auto step = [&](int phase, bool cadence, bool fuse_next, bool next_cadence) -> int {
+    int kk = 0;  // steps issued so far (Nesterov buffer parity / momentum index)
+    auto step = [&](int phase, bool cadence) -> int {
       StepCtl c = ctl;
       c.phase = phase;
       c.defer_commit = cadence ? 1 : 0;
       int r = REDVE_OK;
-      double* fp_this = fpb[kk & 1];
+      double* fp_this = p->fprev.as<double>();
       if (spec) {  // X+ = Xb + m X, cost fused on cadence steps (spectral.cuh)
         SpecStepArgs sa;
         sa.B = B; sa.H = p->H; sa.W = p->W; sa.cur = cur; sa.nxt = nxt; sa.k = sk;
@@ -1499,16 +1484,6 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         ga.partials = p->part_grad.as<double>(); ga.counters = p->cnt_grad.as<unsigned>();
         RUN(ctx, "grad_step", launch_grad_step(ga, s));
         CKL();
-      } else if (p->fourier && fused) {  // one clustered kernel per step (fused.cu)
-        FusedArgs fa;
-        memset(&fa, 0, sizeof(fa));
-        fa.B = B; fa.xin = cur; fa.dn = dn; fa.fout = cadence ? fp_this : nullptr;
-        fa.tws = p->twsW; fa.g = p->g.as<double>(); fa.scale = p->alpha;
-        fa.out = nxt; fa.base = p->xb.as<double>(); fa.xprev = cur; fa.S = S;
-        fa.st = st; fa.ctl = c; fa.tr = tr;
-        fa.partials = p->partials.as<double>(); fa.counters = p->cnt_inv.as<unsigned>();
-        RUN(ctx, "fused_step", launch_fused_step(fa, p->npairs, s));
-        CKL();
       } else if (p->fourier) {
         {
           View xin = cur;
@@ -1524,26 +1499,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
           }
           f_ready = false;
           double* fout = (cadence && !pw) ? fp_this : nullptr;
-          if (!z_ready && (r = f_row_fwd(p, xin, d, zcur, phase, fout))) return r;
+          if ((r = f_row_fwd(p, xin, d, zcur, phase, fout))) return r;
         }
         if ((r = f_col(p, zcur, p->alpha, phase))) return r;
-        if (mid && fuse_next) {
-          RowMidArgs ma;
-          memset(&ma, 0, sizeof(ma));
-          ma.B = B; ma.H = p->H; ma.W = p->W; ma.lpc = p->lpc_row;
-          ma.Zin = zcur; ma.out = nxt; ma.base = p->xb.as<double>(); ma.xprev = cur; ma.S = S;
-          ma.st = st; ma.ctl = c; ma.tr = tr;
-          ma.partials = p->partials.as<double>(); ma.counters = p->cnt_inv.as<unsigned>();
-          ma.dn = dn; ma.Zout = zalt; ma.fout = next_cadence ? fpb[(kk + 1) & 1] : nullptr;
-          ma.tws = p->twsW;
-          RUN(ctx, "row_mid", launch_row_mid(ma, p->npairs, s));
-          CKL();
-          std::swap(zcur, zalt);
-          z_ready = true;
-        } else {
-          r = f_row_inv(p, zcur, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
-          z_ready = false;
-        }
+        r = f_row_inv(p, zcur, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
       } else {
         r = fp_step_cg(p, cur, nxt, phase, nullptr);
         if (r) return r;
@@ -1580,8 +1539,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     int k = 0;
     if (!ve) {
       while (k < budget) {
-        int r = step(PH_MAIN, ((k + 1) % log_every) == 0, k + 1 < budget,
-                     ((k + 2) % log_every) == 0);
+        int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
         if (r) return r;
         ++k;
         if (!use_graph && k % (check_every * clen) == 0 && k < budget) {
@@ -1595,8 +1553,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       while (true) {
         int n = 0;
         for (int i = 0; i < clen; ++i) {
-          int r = step(PH_MAIN, ((k + 1) % log_every) == 0, i + 1 < clen && k + 1 < budget,
-                       ((k + 2) % log_every) == 0);
+          int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
           if (r) return r;
           ++k;
           ++n;
@@ -1622,7 +1579,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
     }
     for (int i = 0; i < stab; ++i) {
-      int r = step(PH_STAB, true, i + 1 < stab, true);
+      int r = step(PH_STAB, true);
       if (r) return r;
     }
     if (track) {  // finalize (solvers.py:255-262)

@@ -407,201 +407,6 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
   }
 }
 
-// --------------------------------------------------------------- row inverse + forward
-// One row pass instead of two: CTA rows [r0, r0+lpc) plus R halo rows on each
-// side go through the inverse row FFT of step k, get x_b added (own rows are
-// written to the ring and feed the step-norm record), then the denoiser of
-// step k+1 runs on the x_{k+1} tile still in shared memory and its rows are
-// transformed forward into a second spectrum buffer.  The halo rows' inverse
-// transforms are recomputed by both neighbours (R/lpc extra FFT work) instead
-// of re-reading x_{k+1} from HBM.
-template <int LW, int DK>
-__global__ void __launch_bounds__(256) k_row_mid(RowMidArgs a) {
-  const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const int phase = a.ctl.phase;
-  const bool a0 = takes_step(a.st[b0], phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
-  if (!a0 && !a1) return;
-  constexpr int W = LW, T = LW / 16;
-  const int H = a.H;
-  const long long N = (long long)H * W;
-  const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
-  const int ks = DK == DN_CONV ? a.dn.ksize : 0;
-  constexpr int ntw = tw_stage_size(LW);
-  cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  double* s_taps = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)));
-  double* s_red = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)) +
-                                            al16f((size_t)ks * ks * sizeof(double)));
-  cd* s_work = reinterpret_cast<cd*>(reinterpret_cast<unsigned char*>(s_red) +
-                                     al16f(32 * 6 * sizeof(double)));
-  if (threadIdx.x < 4) {  // the epilogue's x_b / x_prev rows head for L2 during the FFT
-    const int r0p = blockIdx.x * a.lpc;
-    const int nr = min(a.lpc, H - r0p);
-    const int bi = (threadIdx.x & 1) ? b1 : b0;
-    const bool act = (threadIdx.x & 1) ? a1 : a0;
-    const double* src = act ? ((threadIdx.x < 2) ? a.base + (long long)bi * N : a.xprev.at(bi, a.st))
-                            : nullptr;
-    if (src)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (long long)r0p * W),
-                   "r"((unsigned)(nr * W * sizeof(double))) : "memory");
-  }
-  load_twiddles(s_tw, a.tws, ntw);
-  if (DK == DN_CONV)
-    for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
-  const int line = threadIdx.x / T, t = threadIdx.x - line * T;  // line in [0, lpc + 2R)
-  const int r0 = blockIdx.x * a.lpc;
-  const int grow = wrap_fast(r0 - R + line, H);
-  const bool own = line >= R && line < R + a.lpc && r0 + line - R < H;
-  const cd* zr = a.Zin + ((long long)p * H + grow) * W;
-  cd v[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = ld_cd(zr + t + T * m);
-  __syncthreads();
-  const RowLayout lay{RowLayout::stride_for(W)};
-  line_fft_ct<LW, true>(v, s_work, s_tw, t, line, lay);
-
-  // + x_b -> x_{k+1}; own rows to the ring and into the step-norm partials
-  double acc[6] = {0, 0, 0, 0, 0, 0};
-  {
-    double* o0 = (own && a0) ? a.out.at(b0, a.st) + (long long)grow * W : nullptr;
-    double* o1 = (own && a1) ? a.out.at(b1, a.st) + (long long)grow * W : nullptr;
-    const double* p0 = o0 ? a.xprev.at(b0, a.st) + (long long)grow * W : nullptr;
-    const double* p1 = o1 ? a.xprev.at(b1, a.st) + (long long)grow * W : nullptr;
-    const double* bs0 = a0 ? a.base + (long long)b0 * N + (long long)grow * W : nullptr;
-    const double* bs1 = a1 ? a.base + (long long)b1 * N + (long long)grow * W : nullptr;
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      double lb0[4], lb1[4], lp0[4], lp1[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = t + T * (4 * h + q);
-        lb0[q] = bs0 ? __ldg(bs0 + c) : 0.0;
-        lb1[q] = bs1 ? __ldg(bs1 + c) : 0.0;
-        lp0[q] = p0 ? __ldg(p0 + c) : 0.0;
-        lp1[q] = p1 ? __ldg(p1 + c) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int m = 4 * h + q;
-        const int c = t + T * m;
-        const double val0 = v[m].x + lb0[q], val1 = v[m].y + lb1[q];
-        v[m] = cd{val0, val1};
-        if (o0) {
-          o0[c] = val0;
-          const double d = val0 - lp0[q];
-          acc[0] = fma(d, d, acc[0]);
-          acc[1] = fma(lp0[q], lp0[q], acc[1]);
-          acc[2] += isfinite(val0) ? 0.0 : 1.0;
-        }
-        if (o1) {
-          o1[c] = val1;
-          const double d = val1 - lp1[q];
-          acc[3] = fma(d, d, acc[3]);
-          acc[4] = fma(lp1[q], lp1[q], acc[4]);
-          acc[5] += isfinite(val1) ? 0.0 : 1.0;
-        }
-      }
-    }
-  }
-  // x_{k+1} tile (own + halo rows) for the step k+1 denoiser; every thread has
-  // passed the transform's last barrier, so the line buffers are free
-  const TileLayout tl{RowLayout::stride_for(W)};
-#pragma unroll
-  for (int m = 0; m < 16; ++m) st_cd(s_work + tl.at(line, t + T * m), v[m]);
-  __syncthreads();
-  const bool fwd = line < a.lpc && r0 + line < H;
-  cd f[16];
-  if (fwd) {
-    denoise_span<DK>(f, s_work, tl, line + R, 16 * t, ks, s_taps,
-                     [&](int c) { return edge_wrap(c, W); });
-  }
-  __syncthreads();  // tile consumed: its first lpc rows become the line buffers
-  if (fwd) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) st_cd(s_work + lay.at(line, 16 * t + j), f[j]);
-  }
-  __syncthreads();
-  if (a.fout) {  // f(x_{k+1}) for the cost identity of step k+1, coalesced
-    const int nl = min(a.lpc, H - r0);
-    for (int idx = threadIdx.x; idx < nl * W; idx += blockDim.x) {
-      const int l = idx / W, c = idx - l * W;
-      const cd fv = ld_cd(s_work + lay.at(l, c));
-      const long long o = (long long)(r0 + l) * W + c;
-      if (a0) a.fout[(long long)b0 * N + o] = fv.x;
-      if (a1) a.fout[(long long)b1 * N + o] = fv.y;
-    }
-  }
-  line_fft_ct<LW, false, true>(v, s_work, s_tw, t, line, lay);  // halo lines: discarded
-  if (fwd) {
-    cd* zo = a.Zout + ((long long)p * H + r0 + line) * W;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) st_cd(zo + t + T * m, v[m]);
-  }
-
-  block_sum<6>(acc, s_red);
-  const int nblk = gridDim.x;
-  if (threadIdx.x == 0) {
-    double* dst = a.partials + ((long long)p * nblk + blockIdx.x) * 6;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) dst[i] = acc[i];
-  }
-  __shared__ int s_last;
-  const bool lastb = last_block_of_group(a.counters + p, nblk, &s_last);
-  double tot[6];
-  if (lastb) gather_partials<6>(a.partials + (long long)p * nblk * 6, nblk, tot, s_red);
-  if (lastb && threadIdx.x == 0) {
-    if (a0) record_step(a.st[b0], b0, tot[0], tot[1], tot[2], a.S, a.ctl, a.tr);
-    if (a1) record_step(a.st[b1], b1, tot[3], tot[4], tot[5], a.S, a.ctl, a.tr);
-  }
-}
-
-static size_t row_mid_smem(int W, int lpc, int R, int ks) {
-  return tw_bytes(W) + al16f((size_t)ks * ks * sizeof(double)) + al16f(32 * 6 * sizeof(double)) +
-         (size_t)(lpc + 2 * R) * RowLayout::stride_for(W) * sizeof(cd);
-}
-
-bool row_mid_ok(int H, int W, const DenoiseArgs& dn, int lpc) {
-  // opt-in (REDVE_ROWMID=1): saves the x_{k+1} re-read but measured slower on
-  // configs[1] (94 us vs 36 + 31 us for row_inv + row_fwd: 15 warps per SM,
-  // the epilogue's loads exposed between two transforms) -- see DESIGN.md
-  const char* e = getenv("REDVE_ROWMID");
-  if (!(e && e[0] == '1')) return false;
-  if (W != 64 && W != 128 && W != 256 && W != 512 && W != 1024) return false;
-  if (dn.kind != DN_MEDIAN3 && dn.kind != DN_CONV && dn.kind != DN_IDENTITY) return false;
-  const int R = dn.kind == DN_CONV ? dn.ksize / 2 : (dn.kind == DN_MEDIAN3 ? 1 : 0);
-  if (H < lpc + 2 * R || (lpc + 2 * R) * (W / 16) > 256) return false;
-  return row_mid_smem(W, lpc, R, dn.kind == DN_CONV ? dn.ksize : 0) <= 200 * 1024;
-}
-
-template <int LW, int DK>
-static void row_mid_t(const RowMidArgs& a, int npairs, cudaStream_t s) {
-  static bool done = false;
-  big_smem_once(k_row_mid<LW, DK>, done);
-  const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
-  const int ks = DK == DN_CONV ? a.dn.ksize : 0;
-  dim3 grid(cdivf(a.H, a.lpc), npairs);
-  k_row_mid<LW, DK><<<grid, (a.lpc + 2 * R) * (LW / 16), row_mid_smem(LW, a.lpc, R, ks), s>>>(a);
-}
-
-template <int DK>
-static void row_mid_dk(const RowMidArgs& a, int npairs, cudaStream_t s) {
-  switch (a.W) {
-    case 64: row_mid_t<64, DK>(a, npairs, s); break;
-    case 128: row_mid_t<128, DK>(a, npairs, s); break;
-    case 256: row_mid_t<256, DK>(a, npairs, s); break;
-    case 512: row_mid_t<512, DK>(a, npairs, s); break;
-    default: row_mid_t<1024, DK>(a, npairs, s); break;
-  }
-}
-
-void launch_row_mid(const RowMidArgs& a, int npairs, cudaStream_t s) {
-  switch (a.dn.kind) {
-    case DN_MEDIAN3: row_mid_dk<DN_MEDIAN3>(a, npairs, s); break;
-    case DN_CONV: row_mid_dk<DN_CONV>(a, npairs, s); break;
-    default: row_mid_dk<DN_IDENTITY>(a, npairs, s); break;
-  }
-}
-
 template <int LW>
 static void row_inv_t(const RowInvArgs& a, int npairs, cudaStream_t s) {
   static bool done = false;

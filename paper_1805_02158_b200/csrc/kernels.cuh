@@ -48,27 +48,6 @@ struct RowInvArgs {
   unsigned* counters;
 };
 
-// Inverse row pass of step k fused with the forward row pass of step k+1
-// (fourier.cu k_row_mid): x_{k+1} rows, +halo rows for the denoiser, stay on
-// chip between the two transforms.
-struct RowMidArgs {
-  int B, H, W, lpc;
-  const cd* Zin;       // step k column-pass output
-  View out;            // x_{k+1} (ring)
-  const double* base;  // x_b
-  View xprev;          // x_k (step norm)
-  int S;
-  ImgState* st;
-  StepCtl ctl;         // step k
-  TraceBufs tr;
-  double* partials;
-  unsigned* counters;
-  DenoiseArgs dn;      // step k+1 denoiser
-  cd* Zout;            // step k+1 row spectra (a different buffer than Zin)
-  double* fout;        // optional f(x_{k+1}) (step k+1 is a cost-cadence step)
-  const cd* tws;
-};
-
 enum CostMode : int { COST_RECORD = 0, COST_INIT = 1, COST_FINAL = 2, COST_VALUE = 3 };
 
 struct CostArgs {
@@ -171,8 +150,6 @@ void launch_inv_denom(double* g, int H, int W, const double* taps, int hk, doubl
 size_t row_fwd_smem(int W, int lpc, int radius, int ksize);
 size_t col_smem(int H, int lpc);
 size_t row_inv_smem(int W, int lpc);
-bool row_mid_ok(int H, int W, const DenoiseArgs& dn, int lpc);
-void launch_row_mid(const RowMidArgs& a, int npairs, cudaStream_t s);
 void launch_row_fwd(const RowFwdArgs& a, int npairs, cudaStream_t s);
 void launch_col(const ColArgs& a, int npairs, cudaStream_t s);
 void launch_row_inv(const RowInvArgs& a, int npairs, cudaStream_t s);

@@ -526,54 +526,3 @@ class TestFilterBank:
             assert rel(X[b].ravel(), xo) <= 1e-5
             np.testing.assert_allclose(traces[b].costs(), tro.as_arrays()["cost"], rtol=1e-9)
 
-
-# --------------------------------------------------------------------- fused step (opt-in)
-class TestFusedStep:
-    def test_fused_cluster_step_matches_pipeline(self, rv, monkeypatch):
-        """The opt-in one-kernel cluster step (fused.cu, REDVE_FUSED=1) gives the
-        three-kernel pipeline's solve to rounding."""
-        from paper_1805_02158_b200.synth import voronoi_scene
-
-        n, B = 256, 4
-        op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
-        truths = np.stack([voronoi_scene(s + 3, n) for s in range(B)])
-        clean = np.asarray(op.apply(truths))
-        ys = np.stack([clean[b] + rv.gaussian_noise((n, n), SQRT2, b) for b in range(B)])
-        cfg = rv.SolveConfig(method="fp-ve", ve_method="mpe", max_inner_steps=30)
-        out = {}
-        for flag in ("0", "1"):
-            monkeypatch.setenv("REDVE_FUSED", flag)
-            batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.Median3(), truths)
-            X, traces = rv.solve_batch(batch, ys, cfg)
-            out[flag] = (X.cpu().numpy(), [t.costs() for t in traces])
-        assert rel(out["1"][0], out["0"][0]) <= 1e-11
-        for a, b in zip(out["1"][1], out["0"][1]):
-            np.testing.assert_allclose(a, b, rtol=1e-11)
-
-
-class TestRowMid:
-    def test_row_mid_matches_pipeline(self, rv, monkeypatch):
-        """The opt-in fused inverse+forward row pass (k_row_mid, REDVE_ROWMID=1)
-        reproduces the three-kernel schedule, including cost-cadence steps."""
-        from paper_1805_02158_b200.synth import voronoi_scene
-
-        n, B = 128, 6
-        op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
-        truths = np.stack([voronoi_scene(s + 5, n) for s in range(B)])
-        clean = np.asarray(op.apply(truths))
-        ys = np.stack([clean[b] + rv.gaussian_noise((n, n), SQRT2, b) for b in range(B)])
-        out = {}
-        for flag in ("0", "1"):
-            monkeypatch.setenv("REDVE_ROWMID", flag)
-            for den in (rv.Median3(), rv.GaussianFilter()):
-                for method in ("fp", "fp-ve"):
-                    cfg = rv.SolveConfig(method=method, ve_method="rre", max_inner_steps=26,
-                                         stabilization_iters=2 if method == "fp-ve" else 0)
-                    batch = rv.RedBatch(op, ys, SQRT2, 0.02, den, truths)
-                    X, traces = rv.solve_batch(batch, ys, cfg)
-                    out[(flag, den.name, method)] = (X.cpu().numpy(), [t.costs() for t in traces])
-        for key in [k for k in out if k[0] == "1"]:
-            ref = out[("0",) + key[1:]]
-            assert rel(out[key][0], ref[0]) <= 1e-11, key
-            for a, b in zip(out[key][1], ref[1]):
-                np.testing.assert_allclose(a, b, rtol=1e-11)
