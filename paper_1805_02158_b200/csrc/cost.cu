@@ -243,10 +243,10 @@ bool cost_fp_ok(const CostArgs& a) {
          (a.dn.kind != DN_CONV || a.dn.ksize <= 7);
 }
 
-static int cost_fp_chunks(int B, long long N) {
-  // one wave at the kernel's 4 CTAs/SM (64 registers): 1216 CTAs for B = 64
-  // left a 3rd wave of 32 CTAs (47 us); 576 CTAs: 44 us
-  int c = 592 / B;
+static int cost_fp_chunks(int B, long long N, int wave) {
+  // one wave at the kernel's residency (4 CTAs/SM x 148 SMs at 64 registers):
+  // 1216 CTAs for B = 64 left a 3rd wave of 32 CTAs (47 us); 576 CTAs: 44 us
+  int c = wave / B;
   const long long per = (N / 2 + 255) / 256;  // CTA-passes per image
   if (c > per) c = (int)per;
   if (c > 64) c = 64;
@@ -336,7 +336,16 @@ __global__ void __launch_bounds__(256) k_cost_fp(CostArgs a) {
 
 template <int DK>
 static void cost_fp_t(const CostArgs& a, cudaStream_t s) {
-  dim3 grid(cost_fp_chunks(a.B, (long long)a.H * a.W), a.B);
+  // resident CTAs of this instantiation on this device, queried once
+  static int wave = 0;
+  if (wave == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cost_fp<DK>, 256, 0);
+    wave = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  dim3 grid(cost_fp_chunks(a.B, (long long)a.H * a.W, wave), a.B);
   k_cost_fp<DK><<<grid, 256, 0, s>>>(a);
 }
 

@@ -33,8 +33,8 @@ def solve_sharded(forward, ys, sigma, alpha, denoiser, x0, config, references=No
                   gather: bool = False, solve_fn=None):
     """Solve the rank's block of a global batch.
 
-    ``ys`` / ``x0`` / ``references`` hold the GLOBAL batch (host arrays) or just
-    this rank's block if their length already equals the block size.  Returns
+    ``ys`` / ``x0`` / ``references`` hold the GLOBAL batch (host arrays); every
+    rank slices its own contiguous block ``[lo:hi)`` out of them.  Returns
     ``(lo, hi, x_local, traces_local, status_local)``; with ``gather=True``
     rank 0 additionally receives ``(x_all, status_all)`` (numpy) as element 5.
 
