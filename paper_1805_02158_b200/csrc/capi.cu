@@ -129,6 +129,7 @@ struct redve_ctx {
       ve_q, ve_trace;
   std::vector<double> taps_host;  // what scratch_taps holds (skip identical re-uploads)
   void* taps_dev = nullptr;
+  bool taps_sep = false;          // scratch_taps is followed by the rank-one [u | v]
   ~redve_ctx() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -420,6 +421,7 @@ static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const do
   a.inv_sigma2 = 1.0 / (p->sigma * p->sigma); a.alpha = p->alpha;
   a.rtol = 1e-6; a.abort = 1e-4; a.maxiter = 200; a.it = 0;  // objective.py:35-37
   a.row0 = 0; a.Hg = 0;
+  a.huv = p->separable ? p->hsep.as<double>() : nullptr;
   a.xin = xin; a.xout = xout;
   a.hty = p->hty.as<double>(); a.f = f_ext ? f_ext : p->fbuf.as<double>();
   a.r = p->cr.as<double>(); a.p = p->cp.as<double>(); a.q = p->cq.as<double>();
@@ -523,15 +525,42 @@ int redve_synchronize(redve_ctx* ctx) {
   return REDVE_OK;
 }
 
-// k x k host taps into scratch_taps; identical taps already resident are not
-// re-sent (a pageable upload would serialise the stream with the host)
+// Rank-one PSF?  taps[a][b] == u[a] v[b] to 1e-15 of the largest tap (the
+// uniform and Gaussian kernels are); uv = [u | v], v normalised at the peak.
+static bool rank_one_split(const double* taps, int k, std::vector<double>& uv) {
+  int a0 = 0, b0 = 0;
+  double best = -1.0;
+  for (int a = 0; a < k; ++a)
+    for (int b = 0; b < k; ++b)
+      if (std::fabs(taps[a * k + b]) > best) {
+        best = std::fabs(taps[a * k + b]);
+        a0 = a;
+        b0 = b;
+      }
+  uv.assign(2 * k, 0.0);
+  if (!(best > 0) || k <= 1) return false;
+  for (int a = 0; a < k; ++a) uv[a] = taps[a * k + b0];
+  for (int b = 0; b < k; ++b) uv[k + b] = taps[a0 * k + b] / taps[a0 * k + b0];
+  for (int a = 0; a < k; ++a)
+    for (int b = 0; b < k; ++b)
+      if (std::fabs(uv[a] * uv[k + b] - taps[a * k + b]) > 1e-15 * best) return false;
+  return true;
+}
+
+// k x k host taps into scratch_taps (followed by [u | v] when rank one);
+// identical taps already resident are not re-sent (a pageable upload would
+// serialise the stream with the host)
 static int put_taps(redve_ctx* ctx, const double* taps, int k) {
   const size_t n = (size_t)k * k, kb = sizeof(double) * n;
-  CK(ctx->scratch_taps.ensure(kb));
+  CK(ctx->scratch_taps.ensure(kb + sizeof(double) * 2 * k));
   if (ctx->taps_dev == ctx->scratch_taps.p && ctx->taps_host.size() == n &&
       memcmp(ctx->taps_host.data(), taps, kb) == 0)
     return REDVE_OK;
-  CK(cudaMemcpyAsync(ctx->scratch_taps.p, taps, kb, cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<double> buf(taps, taps + n), uv;
+  ctx->taps_sep = rank_one_split(taps, k, uv);
+  buf.insert(buf.end(), uv.begin(), uv.end());
+  CK(cudaMemcpyAsync(ctx->scratch_taps.p, buf.data(), sizeof(double) * buf.size(),
+                     cudaMemcpyHostToDevice, ctx->stream));
   ctx->taps_host.assign(taps, taps + n);
   ctx->taps_dev = ctx->scratch_taps.p;
   return REDVE_OK;
@@ -785,22 +814,8 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   PK(cudaMemcpyAsync(p->htaps.p, op->taps, kb, cudaMemcpyHostToDevice, s));
   {  // rank-one PSF? taps[a][b] == u[a] v[b] (uniform and Gaussian kernels are)
     const int k = op->ksize;
-    int a0 = 0, b0 = 0;
-    double best = -1.0;
-    for (int a = 0; a < k; ++a)
-      for (int b = 0; b < k; ++b)
-        if (std::fabs(op->taps[a * k + b]) > best) {
-          best = std::fabs(op->taps[a * k + b]);
-          a0 = a;
-          b0 = b;
-        }
-    std::vector<double> uv(2 * k);
-    for (int a = 0; a < k; ++a) uv[a] = op->taps[a * k + b0];
-    for (int b = 0; b < k; ++b) uv[k + b] = op->taps[a0 * k + b] / op->taps[a0 * k + b0];
-    bool sep = best > 0;
-    for (int a = 0; a < k && sep; ++a)
-      for (int b = 0; b < k && sep; ++b)
-        sep = std::fabs(uv[a] * uv[k + b] - op->taps[a * k + b]) <= 1e-15 * best;
+    std::vector<double> uv;
+    const bool sep = rank_one_split(op->taps, k, uv);
     if (sep && k > 1) {
       p->separable = 1;
       PK(p->hsep.ensure(sizeof(double) * 2 * k));
@@ -1029,6 +1044,7 @@ int redve_gradient(redve_problem* p, const double* x, const double* f_ext, doubl
     ca.B = p->B; ca.H = p->H; ca.W = p->W; ca.factor = p->op.factor; ca.k = p->op.ksize;
     ca.taps = p->htaps.as<double>();
     ca.inv_sigma2 = 1.0 / (p->sigma * p->sigma); ca.alpha = p->alpha;
+    ca.huv = p->separable ? p->hsep.as<double>() : nullptr;
     ca.xin = xv; ca.q = p->cq.as<double>(); ca.cg = p->cgst.as<CgState>();
     ca.st = p->state.as<ImgState>(); ca.phase = PH_SETUP;
     RUN(ctx, "normal_matvec", launch_normal_matvec(ca, s));
@@ -1461,6 +1477,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
           ca.B = B; ca.H = p->H; ca.W = p->W; ca.factor = p->op.factor; ca.k = p->op.ksize;
           ca.taps = p->htaps.as<double>();
           ca.inv_sigma2 = 1.0 / (p->sigma * p->sigma); ca.alpha = p->alpha;
+          ca.huv = p->separable ? p->hsep.as<double>() : nullptr;
           ca.xin = vin; ca.q = p->cq.as<double>(); ca.cg = p->cgst.as<CgState>(); ca.st = st;
           ca.phase = phase;
           RUN(ctx, "normal_matvec", launch_normal_matvec(ca, s));
@@ -1814,6 +1831,7 @@ int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double
   memset(&a, 0, sizeof(a));
   a.B = 1; a.H = Hext; a.W = W; a.factor = op->factor; a.k = op->ksize;
   a.taps = ctx->scratch_taps.as<double>();
+  a.huv = ctx->taps_sep ? a.taps + (size_t)op->ksize * op->ksize : nullptr;
   a.inv_sigma2 = 1.0 / (sigma * sigma); a.alpha = alpha;
   a.row0 = row0; a.Hg = Hg;
   a.xin = plain(w, (long long)Hext * W);

@@ -552,6 +552,28 @@ void launch_pw(const PwArgs& a_in, cudaStream_t s, int* launches) {
 // (a compact lattice list, periodic seams included), and each output gathers
 // the <= ceil((2r+1)/s)^2 lattice samples in its window -- the same terms, in
 // the same order, as the dense correlation with the zero-filled z_up.
+// the matvec passes' reduced sums -> CG state (scipy cg, iterative.py:384-430)
+template <int MODE>
+__device__ __forceinline__ void cg_reduce_finish(CgState& cs, const CgArgs& a, int b, double t0,
+                                                 double t1) {
+  if (MODE == CG_ITER) {
+    cs.alpha = cs.rho / t0;  // rho_cur / (p . q)
+  } else if (MODE == CG_INIT) {
+    const double bn = sqrt(t0);
+    cs.bn2 = t0;
+    cs.atol = a.rtol * bn;  // max(atol=0, rtol*||b||)
+    cs.rho = t1;
+    cs.its = 0;
+    cs.info = 0;
+    cs.need_resid = 0;
+    cs.zero_b = (bn == 0.0);
+    cs.active = !(cs.zero_b || sqrt(t1) < cs.atol);
+  } else {  // residual check after maxiter (objective.py:114-120)
+    if (sqrt(t1) > a.abort * sqrt(t0)) a.st[b].err = ERR_CG;
+    cs.need_resid = 0;
+  }
+}
+
 constexpr int MV_TH = 32, MV_TW = 32;
 
 template <int MODE>
@@ -695,25 +717,453 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
   const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
   double tt[2];
   if (lastb) gather_partials<2>(a.partials + (long long)b * nblk * 2, nblk, tt, red);
-  if (lastb && threadIdx.x == 0) {
-    const double t0 = tt[0], t1 = tt[1];
-    if (MODE == CG_ITER) {
-      cs.alpha = cs.rho / t0;  // rho_cur / (p . q)
-    } else if (MODE == CG_INIT) {
-      const double bn = sqrt(t0);
-      cs.bn2 = t0;
-      cs.atol = a.rtol * bn;  // max(atol=0, rtol*||b||)
-      cs.rho = t1;
-      cs.its = 0;
-      cs.info = 0;
-      cs.need_resid = 0;
-      cs.zero_b = (bn == 0.0);
-      cs.active = !(cs.zero_b || sqrt(t1) < cs.atol);
-    } else {  // residual check after maxiter (objective.py:114-120)
-      if (sqrt(t1) > a.abort * sqrt(t0)) a.st[b].err = ERR_CG;
-      cs.need_resid = 0;
+  if (lastb && threadIdx.x == 0) cg_reduce_finish<MODE>(cs, a, b, tt[0], tt[1]);
+}
+
+// Compile-time operator (7 x 7 PSF, factor 3: configs[2]/[4]).  Same terms in
+// the same order as k_cg_matvec (bit-identical results), organised by the
+// lattice's 3 x 3 phases:
+//  * tiles of 24 x 96 outputs start on lattice rows / columns (the host picks
+//    the row offset of the slab's larger lattice-regular region), so in a
+//    tile away from a periodic seam the lattice is every 3rd window row and
+//    column;
+//  * there every lane owns a 3-column triple and every warp a row triple:
+//    the 3 x 3 lattice samples of a triple pair sit in registers and its 9
+//    outputs contract them with compile-time tap indices (49 MACs, taps
+//    warp-uniform, z reads conflict-free);
+//  * tiles whose window crosses a seam (lattice spacing 1 or 2) take the
+//    list-based path: lattice rows / columns compacted by warp ballots, each
+//    output row / column building its <= 4 (sample, tap) pairs in parallel.
+//  * a rank-one PSF (u v^T: the Gaussian of configs[2]/[4]) contracts both
+//    stages as two 1-D passes in regular tiles: z = u * (v * w) at the
+//    lattice, H^T z = u * (v * z) at the outputs -- 2.5x fewer shared loads,
+//    1.6x fewer FMAs; the terms regrouped, equal to the 2-D sums to rounding.
+constexpr int MVP_TH = 24, MVP_TW = 96, MVP_MAXL = 4;
+
+struct MvpGeom {
+  static constexpr int K = 7, S = 3, R = 3;
+  static constexpr int HX = MVP_TH + 4 * R, WX = MVP_TW + 4 * R;  // w tile
+  static constexpr int HZ = MVP_TH + 2 * R, WZ = MVP_TW + 2 * R;  // z_up window
+  // lattice rows / columns in a window: spacing S except one periodic seam
+  static constexpr int NZR = HZ / S + 2, NZC = WZ / S + 2;
+  static constexpr int NLR = HZ / S, NLC = WZ / S;  // regular tiles
+  static constexpr int KK = (K * K + 1) & ~1;       // taps, padded: the w tile 16-byte aligned
+  static constexpr int HR = S * (NLR - 1) + K;      // window rows the lattice samples read
+  static constexpr int NHS = HR * NLC > NLR * MVP_TW ? HR * NLC : NLR * MVP_TW;
+  static constexpr int NINT = NZR + NZC + HZ + WZ + (MVP_TH + MVP_TW) * (MVP_MAXL + 1) + 4;
+  // taps | w tile | z | rank-one passes | reduction scratch | index lists
+  static constexpr size_t smem =
+      sizeof(double) * ((size_t)KK + (size_t)HX * WX + (size_t)NZR * NZC + NHS + 64) +
+      sizeof(int) * (size_t)NINT;
+};
+
+// output phase p (0..2) of a triple: its lattice samples d (0..2, ascending)
+// and tap indices t; phase 0 uses all three, phases 1 / 2 the last two
+__device__ __forceinline__ constexpr int mvp_tap(int p, int d) {
+  return p == 0 ? 3 * d : (p == 1 ? 3 * d - 1 : 3 * d - 2);
+}
+
+// the shared-memory scratch of one tile's contraction
+struct MvpSmem {
+  const double* taps;
+  double* zc;
+  double* hs;  // rank-one PSF: row pass at the lattice columns, then the column pass
+  int* ints;   // zr_pos | zc_pos | rcomp | ccomp | rlist | clist | nzr nzc irr
+};
+
+// i in [-n, 2n): periodic index without a division
+__device__ __forceinline__ int wrap_near(int i, int n) {
+  return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
+template <int MODE>
+__device__ __forceinline__ bool mvp_vec_ok(const CgArgs& a, int j0) {
+  using G = MvpGeom;
+  return (a.W % 2) == 0 && j0 - 2 * G::R >= 0 && j0 - 2 * G::R + G::WX <= a.W;
+}
+
+// Synchronous tile load: 16-byte loads along interior rows, every thread's
+// loads issued before its shared-memory stores (the load is the exposed latency)
+template <int MODE>
+__device__ __forceinline__ void mvp_load(const CgArgs& a, const double* src_x, const double* rr,
+                                         const double* pold, double beta, int i0, int j0,
+                                         double* ws) {
+  using G = MvpGeom;
+  constexpr int R = G::R, HX = G::HX, WX = G::WX;
+  const int H = a.H, W = a.W;
+  if (mvp_vec_ok<MODE>(a, j0)) {
+    constexpr int W2 = WX / 2, ITEMS = HX * W2, PER = (ITEMS + 255) / 256;
+    double2 v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int it = threadIdx.x + 256 * q;
+      const int ti = it / W2, c2 = it - ti * W2;
+      v[q] = make_double2(0.0, 0.0);
+      if (it < ITEMS) {
+        const long long o = (long long)wrap_near(i0 - 2 * R + ti, H) * W + j0 - 2 * R + 2 * c2;
+        if (MODE == CG_ITER) {
+          const double2 rv = *reinterpret_cast<const double2*>(rr + o);
+          if (a.it > 0) {
+            const double2 pv = *reinterpret_cast<const double2*>(pold + o);
+            v[q] = make_double2(fma(beta, pv.x, rv.x), fma(beta, pv.y, rv.y));
+          } else {
+            v[q] = rv;
+          }
+        } else {
+          v[q] = *reinterpret_cast<const double2*>(src_x + o);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int it = threadIdx.x + 256 * q;
+      if (it < ITEMS) *reinterpret_cast<double2*>(ws + 2 * it) = v[q];
+    }
+  } else {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int ti = warp; ti < HX; ti += 8) {
+      const long long ro = (long long)wrap(i0 - 2 * R + ti, H) * W;
+      for (int tj = lane; tj < WX; tj += 32) {
+        const long long o = ro + wrap_fast(j0 - 2 * R + tj, W);
+        double w;
+        if (MODE == CG_ITER) w = (a.it > 0) ? fma(beta, pold[o], rr[o]) : rr[o];
+        else w = src_x[o];
+        ws[ti * WX + tj] = w;
+      }
     }
   }
+}
+
+// Lattice of the tile's window (by GLOBAL row: a slab starts at global row
+// a.row0 of an a.Hg-row image).  A tile (lattice-aligned origin) whose window
+// crosses neither the buffer's wrap nor the global seam has the lattice on
+// exactly the window rows / columns == 0 mod 3 (regular, decided in O(1));
+// otherwise the lattice is compacted by ballots.  Ends on a barrier.
+__device__ __forceinline__ bool mvp_regular(const CgArgs& a, int i0, int j0) {
+  using G = MvpGeom;
+  constexpr int R = G::R, S = G::S;
+  const int lo = i0 - R, hi = i0 + G::HZ - R;  // window rows [lo, hi)
+  if (lo < 0 || hi > a.H || j0 - R < 0 || j0 - R + G::WZ > a.W) return false;
+  // a.seam: local row of global row 0 (-1: none); a.row0m = row0 mod Hg
+  if (a.seam > lo && a.seam < hi) return false;
+  const int g = (a.seam >= 0 && i0 >= a.seam) ? i0 - a.seam : a.row0m + i0;
+  return g % S == 0;
+}
+
+__device__ __forceinline__ bool mvp_lattice(const CgArgs& a, int i0, int j0, const MvpSmem& m) {
+  using G = MvpGeom;
+  constexpr int R = G::R, S = G::S, HZ = G::HZ, WZ = G::WZ;
+  if (mvp_regular(a, i0, j0)) {
+    __syncthreads();
+    return true;
+  }
+  int* zr_pos = m.ints;
+  int* zc_pos = zr_pos + G::NZR;
+  int* rcomp = zc_pos + G::NZC;
+  int* ccomp = rcomp + HZ;
+  int* sc = m.ints + G::NINT - 4;  // nzr, nzc, row irregular, column irregular
+  const int H = a.H, W = a.W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    int base = 0, irr = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int zi = c * 32 + lane;
+      bool on = false;
+      if (zi < HZ) {
+        const int gu = wrap_fast(i0 - R + zi, H);
+        const int gg = (a.Hg > 0) ? (int)(((long long)a.row0 + gu) % a.Hg) : gu;
+        on = (gg % S) == 0;
+        irr |= on != (zi % S == 0);
+      }
+      const unsigned msk = __ballot_sync(0xffffffffu, on);
+      const int idx = base + __popc(msk & ((1u << lane) - 1u));
+      if (zi < HZ) rcomp[zi] = on ? idx : -1;
+      if (on) zr_pos[idx] = zi;
+      base += __popc(msk);
+    }
+    irr = __any_sync(0xffffffffu, irr);
+    if (lane == 0) {
+      sc[0] = base;
+      sc[2] = irr;
+    }
+  } else if (warp == 1) {
+    int base = 0, irr = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int zj = c * 32 + lane;
+      const bool on = zj < WZ && (wrap_fast(j0 - R + zj, W) % S) == 0;
+      irr |= zj < WZ && on != (zj % S == 0);
+      const unsigned msk = __ballot_sync(0xffffffffu, on);
+      const int idx = base + __popc(msk & ((1u << lane) - 1u));
+      if (zj < WZ) ccomp[zj] = on ? idx : -1;
+      if (on) zc_pos[idx] = zj;
+      base += __popc(msk);
+    }
+    irr = __any_sync(0xffffffffu, irr);
+    if (lane == 0) {
+      sc[1] = base;
+      sc[3] = irr;
+    }
+  }
+  __syncthreads();
+  return (sc[2] | sc[3]) == 0;
+}
+
+// (H^T z_up)(u, v) of every output of the tile, handed to emit(oi, oj, ht).
+// Starts after mvp_lattice's barrier with ws complete; ends with every read
+// of ws / zc issued before the caller's next barrier.
+template <class Emit>
+__device__ __forceinline__ void mvp_contract(bool regular, const double* ws, const MvpSmem& m,
+                                             const double* huv, Emit&& emit) {
+  using G = MvpGeom;
+  constexpr int K = G::K, S = G::S, R = G::R, WX = G::WX, NZC = G::NZC, NLC = G::NLC;
+  constexpr int NLR = G::NLR, TH = MVP_TH, TW = MVP_TW, ML = MVP_MAXL;
+  static_assert(G::HZ <= 64 && G::WZ <= 128, "ballot compaction covers 64 rows / 128 columns");
+  static_assert(TH == 24 && TW == 96, "8 warps x a row triple, 32 lanes x a column triple");
+  const double* taps = m.taps;
+  double* zc = m.zc;
+  int* zr_pos = m.ints;
+  int* zc_pos = zr_pos + G::NZR;
+  int* rcomp = zc_pos + NZC;
+  int* ccomp = rcomp + G::HZ;
+  int* rlist = ccomp + G::WZ;  // per output row: ML x (compact index << 8 | tap row), count
+  int* clist = rlist + TH * (ML + 1);
+  const int* sc = m.ints + G::NINT - 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (regular && huv) {
+    double uu[K], vv[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      uu[t] = __ldg(huv + t);
+      vv[t] = __ldg(huv + K + t);
+    }
+    double* hs = m.hs;
+    // h(row, lj) = sum_tb v[tb] w(row, 3 lj + 2r - tb)
+    for (int idx = threadIdx.x; idx < G::HR * NLC; idx += blockDim.x) {
+      const int row = idx / NLC, lj = idx - row * NLC;
+      const double* wp = ws + row * WX + S * lj + 2 * R;
+      double h = 0.0;
+#pragma unroll
+      for (int tb = 0; tb < K; ++tb) h = fma(vv[tb], wp[-tb], h);
+      hs[idx] = h;
+    }
+    __syncthreads();
+    // z(li, lj) = sum_ta u[ta] h(3 li + 2r - ta, lj)
+    for (int idx = threadIdx.x; idx < NLR * NLC; idx += blockDim.x) {
+      const int li = idx / NLC, lj = idx - li * NLC;
+      const double* hp = hs + (S * li + 2 * R) * NLC + lj;
+      double z = 0.0;
+#pragma unroll
+      for (int ta = 0; ta < K; ++ta) z = fma(uu[ta], hp[-ta * NLC], z);
+      zc[idx] = z;
+    }
+    __syncthreads();
+    // g(li, v) = sum_dc v[tap(pv, dc)] z(li, c + dc), v = 3 c + pv (into hs)
+    for (int idx = threadIdx.x; idx < NLR * 32; idx += blockDim.x) {
+      const int li = idx >> 5, c = idx & 31;
+      double z3[3];
+#pragma unroll
+      for (int dc = 0; dc < 3; ++dc) z3[dc] = zc[li * NLC + c + dc];
+#pragma unroll
+      for (int pv = 0; pv < 3; ++pv) {
+        double g = 0.0;
+#pragma unroll
+        for (int dc = pv == 0 ? 0 : 1; dc < 3; ++dc) g = fma(vv[mvp_tap(pv, dc)], z3[dc], g);
+        hs[li * TW + 3 * c + pv] = g;
+      }
+    }
+    __syncthreads();
+    const int tr = warp;
+#pragma unroll
+    for (int pv = 0; pv < 3; ++pv) {
+      double g3[3];
+#pragma unroll
+      for (int da = 0; da < 3; ++da) g3[da] = hs[(tr + da) * TW + 3 * lane + pv];
+#pragma unroll
+      for (int pu = 0; pu < 3; ++pu) {
+        double ht = 0.0;
+#pragma unroll
+        for (int da = pu == 0 ? 0 : 1; da < 3; ++da) ht = fma(uu[mvp_tap(pu, da)], g3[da], ht);
+        emit(3 * tr + pu, 3 * lane + pv, ht);
+      }
+    }
+    return;
+  }
+  if (regular) {
+    // z at lattice (li, lj) = window (3 li, 3 lj)
+    for (int idx = threadIdx.x; idx < NLR * NLC; idx += blockDim.x) {
+      const int li = idx / NLC, lj = idx - li * NLC;
+      const double* wp = ws + (S * li + 2 * R) * WX + (S * lj + 2 * R);
+      double z = 0.0;
+#pragma unroll
+      for (int ta = 0; ta < K; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < K; ++tb) z = fma(taps[ta * K + tb], wp[-ta * WX - tb], z);
+      zc[li * NLC + lj] = z;
+    }
+    __syncthreads();
+    const int tr = warp;
+    double z9[3][3];
+#pragma unroll
+    for (int da = 0; da < 3; ++da)
+#pragma unroll
+      for (int dc = 0; dc < 3; ++dc) z9[da][dc] = zc[(tr + da) * NLC + lane + dc];
+#pragma unroll
+    for (int pu = 0; pu < 3; ++pu)
+#pragma unroll
+      for (int pv = 0; pv < 3; ++pv) {
+        double ht = 0.0;
+#pragma unroll
+        for (int da = pu == 0 ? 0 : 1; da < 3; ++da)
+#pragma unroll
+          for (int dc = pv == 0 ? 0 : 1; dc < 3; ++dc)
+            ht = fma(taps[mvp_tap(pu, da) * K + mvp_tap(pv, dc)], z9[da][dc], ht);
+        emit(3 * tr + pu, 3 * lane + pv, ht);
+      }
+    return;
+  }
+  const int nzr = sc[0], nzc = sc[1];
+  // output row u (tile coords) reads window rows [u, u + 2r]; column v likewise
+  if (threadIdx.x < TH) {
+    const int u = threadIdx.x;
+    int n = 0;
+#pragma unroll
+    for (int d = 0; d <= 2 * R; ++d) {
+      const int c = rcomp[u + d];
+      if (c >= 0 && n < ML) rlist[u * (ML + 1) + (n++)] = (c << 8) | d;
+    }
+    rlist[u * (ML + 1) + ML] = n;
+  } else if (threadIdx.x >= 64 && threadIdx.x < 64 + TW) {
+    const int v = threadIdx.x - 64;
+    int n = 0;
+#pragma unroll
+    for (int d = 0; d <= 2 * R; ++d) {
+      const int c = ccomp[v + d];
+      if (c >= 0 && n < ML) clist[v * (ML + 1) + (n++)] = (c << 8) | d;
+    }
+    clist[v * (ML + 1) + ML] = n;
+  }
+  // z = H w at the lattice samples (taps in the order of k_cg_matvec)
+  for (int idx = threadIdx.x; idx < nzr * nzc; idx += blockDim.x) {
+    const int li = idx / nzc, lj = idx - li * nzc;
+    const double* wp = ws + (zr_pos[li] + 2 * R) * WX + (zc_pos[lj] + 2 * R);
+    double z = 0.0;
+#pragma unroll
+    for (int ta = 0; ta < K; ++ta)
+#pragma unroll
+      for (int tb = 0; tb < K; ++tb) z = fma(taps[ta * K + tb], wp[-ta * WX - tb], z);
+    zc[li * NZC + lj] = z;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TH * TW; idx += blockDim.x) {
+    const int oi = idx / TW, oj = idx - oi * TW;
+    const int* rl = rlist + oi * (ML + 1);
+    const int* cl = clist + oj * (ML + 1);
+    const int rn = rl[ML], cn = cl[ML];
+    int ce[ML];
+#pragma unroll
+    for (int j = 0; j < ML; ++j) ce[j] = cl[j];
+    double ht = 0.0;  // lattice rows then columns ascending
+#pragma unroll
+    for (int i = 0; i < ML; ++i) {
+      if (i < rn) {
+        const int re = rl[i];
+        const double* trow = taps + (re & 255) * K;
+        const double* zrow = zc + (re >> 8) * NZC;
+#pragma unroll
+        for (int j = 0; j < ML; ++j)
+          if (j < cn) ht = fma(trow[ce[j] & 255], zrow[ce[j] >> 8], ht);
+      }
+    }
+    emit(oi, oj, ht);
+  }
+}
+
+__device__ __forceinline__ MvpSmem mvp_smem(double** ws) {
+  using G = MvpGeom;
+  double* base = reinterpret_cast<double*>(s_smem);
+  *ws = base + G::KK;
+  double* zc = *ws + G::HX * G::WX;
+  double* hs = zc + G::NZR * G::NZC;
+  return MvpSmem{base, zc, hs, reinterpret_cast<int*>(hs + G::NHS + 64)};
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) k_cg_matvec_ct(CgArgs a) {
+  using G = MvpGeom;
+  constexpr int R = G::R, WX = G::WX, TH = MVP_TH, TW = MVP_TW;
+  const int b = blockIdx.z;
+  CgState& cs = a.cg[b];
+  if (MODE == CG_INIT) {
+    if (!takes_step(a.st[b], a.phase)) return;
+  } else if (MODE == CG_ITER) {
+    if (!cs.active) return;
+  } else if (MODE == CG_RESID) {
+    if (!takes_step(a.st[b], a.phase) || !cs.need_resid) return;
+  }
+  double* ws;
+  const MvpSmem m = mvp_smem(&ws);
+  double* taps = const_cast<double*>(m.taps);
+  double* red = m.hs + G::NHS;
+  for (int i = threadIdx.x; i < G::K * G::K; i += blockDim.x) taps[i] = a.taps[i];
+  const int H = a.H, W = a.W;
+  const long long N = (long long)H * W;
+  const int i0 = a.tile_off + (blockIdx.y - 1) * TH, j0 = blockIdx.x * TW;
+  const double beta = (MODE == CG_ITER && a.it > 0) ? cs.beta : 0.0;
+  const double* xin = (MODE == CG_ITER) ? nullptr : a.xin.at(b, a.st);
+  mvp_load<MODE>(a, xin, a.r + (long long)b * N, a.p + (long long)b * N, beta, i0, j0, ws);
+  const bool regular = mvp_lattice(a, i0, j0, m);  // its barrier also completes ws
+  double acc[2] = {0.0, 0.0};
+  const double inv_s2 = a.inv_sigma2;
+  mvp_contract(regular, ws, m, a.huv, [&](int oi, int oj, double ht) {
+    const int gi = i0 + oi, gj = j0 + oj;
+    if (gi < 0 || gi >= H || gj >= W) return;
+    const double wv = ws[(oi + 2 * R) * WX + (oj + 2 * R)];
+    const double aw = fma(ht, inv_s2, a.alpha * wv);
+    const long long o = (long long)b * N + (long long)gi * W + gj;
+    if (MODE == CG_PLAIN) {
+      a.q[o] = aw;
+    } else if (MODE == CG_ITER) {
+      a.p[o] = wv;
+      a.q[o] = aw;
+      acc[0] = fma(wv, aw, acc[0]);
+    } else {
+      const double bb = fma(a.alpha, a.f[o], a.hty[o]);  // rhs = H^T y/sigma^2 + alpha f
+      const double res = bb - aw;
+      if (MODE == CG_INIT) {
+        a.r[o] = res;
+        a.xout.at(b, a.st)[(long long)gi * W + gj] = wv;  // warm start copy x <- x_k
+      }
+      acc[0] = fma(bb, bb, acc[0]);
+      acc[1] = fma(res, res, acc[1]);
+    }
+  });
+  if (MODE == CG_PLAIN) return;
+  block_sum<2>(acc, red);
+  const int nblk = gridDim.x * gridDim.y;
+  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) {
+    a.partials[((long long)b * nblk + blk) * 2] = acc[0];
+    a.partials[((long long)b * nblk + blk) * 2 + 1] = acc[1];
+  }
+  __shared__ int s_last;
+  const bool lastb = last_block_of_group(a.counters + b, nblk, &s_last);
+  double tt[2];
+  if (lastb) gather_partials<2>(a.partials + (long long)b * nblk * 2, nblk, tt, red);
+  if (lastb && threadIdx.x == 0) cg_reduce_finish<MODE>(cs, a, b, tt[0], tt[1]);
+}
+
+// Local row of a lattice-aligned tile origin: the lattice phase of the slab's
+// larger regular region (before / after the global periodic seam).
+static int mvp_tile_off(const CgArgs& a) {
+  const int H = a.H;
+  if (a.Hg <= 0) return 0;  // the buffer is the image: lattice rows 0, 3, ...
+  const long long r0 = ((long long)a.row0 % a.Hg + a.Hg) % a.Hg;
+  const int seam = (int)(a.Hg - r0);  // local row of global row 0
+  const int before = (int)((3 - r0 % 3) % 3);
+  if (seam <= 0 || seam >= H) return before;
+  return (seam >= H - seam) ? before : seam % 3;
 }
 
 // x += alpha p ; r -= alpha q ; rho = r.r ; stopping decisions
@@ -778,8 +1228,39 @@ size_t cg_matvec_smem(int k) {
          sizeof(int) * ((size_t)(MV_TH + 2 * r) + (MV_TW + 2 * r) + 2 * MV_TH + 2 * MV_TW + 64);
 }
 
+// REDVE_MATVEC=generic: the runtime-(k, s) kernel for every operator (A/B tests)
+static bool matvec_ct_ok(const CgArgs& a) {
+  const char* e = getenv("REDVE_MATVEC");
+  if (e && e[0] == 'g') return false;
+  return a.k == 7 && a.factor == 3;
+}
+
 template <int MODE>
-static void matvec_t(const CgArgs& a, cudaStream_t s) {
+static void matvec_t(const CgArgs& a_in, cudaStream_t s) {
+  if (matvec_ct_ok(a_in)) {
+    CgArgs a = a_in;
+    a.tile_off = mvp_tile_off(a);
+    if (a.Hg > 0) {
+      const long long r0 = ((long long)a.row0 % a.Hg + a.Hg) % a.Hg;
+      const long long sm = (a.Hg - r0) % a.Hg;  // local row of global row 0
+      a.row0m = (int)r0;
+      a.seam = sm < a.H ? (int)sm : -1;
+    } else {
+      a.row0m = 0;
+      a.seam = -1;
+    }
+    // tile rows start at tile_off - TH (the first covers rows [0, tile_off))
+    const int ntx = cdivs(a.W, MVP_TW), nty = 1 + cdivs(a.H - a.tile_off, MVP_TH);
+    static bool ct_done = false;
+    if (!ct_done) {
+      cudaFuncSetAttribute(k_cg_matvec_ct<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)MvpGeom::smem);
+      ct_done = true;
+    }
+    k_cg_matvec_ct<MODE><<<dim3(ntx, nty, a.B), 256, MvpGeom::smem, s>>>(a);
+    return;
+  }
+  const CgArgs& a = a_in;
   static bool done = false;
   if (!done) {
     cudaFuncSetAttribute(k_cg_matvec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -790,7 +1271,11 @@ static void matvec_t(const CgArgs& a, cudaStream_t s) {
   k_cg_matvec<MODE><<<grid, 256, cg_matvec_smem(a.k), s>>>(a);
 }
 
-int cg_matvec_blocks(int H, int W) { return cdivs(W, MV_TW) * cdivs(H, MV_TH); }
+int cg_matvec_blocks(int H, int W) {  // the larger of both kernels' tile counts
+  const int g = cdivs(W, MV_TW) * cdivs(H, MV_TH);
+  const int c = cdivs(W, MVP_TW) * (2 + cdivs(H, MVP_TH));
+  return g > c ? g : c;
+}
 int cg_update_blocks(long long N) {
   int c = cdivs(N, 256 * 8);
   return c > 1184 ? 1184 : (c < 1 ? 1 : c);

@@ -30,9 +30,12 @@ struct CgState {
 struct CgArgs {
   int B, H, W, factor, k;
   const double* taps;  // device k*k
+  const double* huv;   // rank-one PSF: device [u | v] (k each), else null
   double inv_sigma2, alpha, rtol, abort;
   int maxiter, it;
   int row0, Hg;        // global row of local row 0 / global height (0: the buffer is the image)
+  int tile_off;        // compile-time operator kernel: local row of a lattice-aligned tile origin,
+  int row0m, seam;     // row0 mod Hg, local row of global row 0 (-1: none)  (set by the launcher)
   View xin;            // CG_INIT: x_k ; CG_RESID: the solution
   View xout;           // the solution being built (warm-started copy of x_k)
   const double* hty;   // [B][N] H^T y / sigma^2

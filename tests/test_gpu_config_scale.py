@@ -166,7 +166,11 @@ def test_config2_768_vs_reference(rv, golden, name, method, budget, weights):
     # configs[2] precision); the iterates stay within the 1e-5 bar
     assert err <= (1e-6 if weights == "float64" else 1e-5), err
     np.testing.assert_array_equal(res.cg_iters[0, :budget], g[f"{name}/cg_iters"])
-    cmp_trace(tr, g, name, cost_rtol=1e-9 if weights == "float64" else 1e-6)
+    # Every fixed-point step is a CG solve stopped at ||r|| < 1e-6 ||b|| (scipy's
+    # rtol, objective.py:112-113): operator sums that round differently (FFT in
+    # the reference, the lattice-phase contraction here) land on iterates that
+    # agree to about that residual, so costs agree to ~1e-8, not to fp64 rounding.
+    cmp_trace(tr, g, name, cost_rtol=1e-7 if weights == "float64" else 1e-6)
 
 
 # ----------------------------------------------------------------- configs[3]
