@@ -6,6 +6,7 @@ neighbours: the last slab's bottom halo is the first slab's top rows, the
 reference's all-periodic boundary, imaging.py:8-9).  Per fixed-point step:
 
 * one halo exchange of x (reach of the denoiser and of the normal operator);
+  the CG direction p exchanges only the normal operator's reach (2r rows);
 * the denoiser on the extended slab (its result is exact on the interior
   rows because the halo covers the denoiser's reach);
 * conjugate gradients with scipy's semantics (iterative.py:311-430) on the
@@ -260,6 +261,9 @@ class SpatialProblem:
         r = forward.psf.radius
         halo = max(denoiser_reach(denoiser) if reach is None else int(reach), 2 * r)
         self.lay = SlabLayout(H, W, self.s, self.comm.world, self.comm.rank, halo)
+        # the normal operator's reach (H^T H: 2r rows): the CG direction p only
+        # needs these rows from the neighbours, not the denoiser's halo
+        self.op_lay = SlabLayout(H, W, self.s, self.comm.world, self.comm.rank, 2 * r)
         lay = self.lay
         y = np.asarray(y, dtype=np.float64)
         # zero-filled upsampling of the slab's measurement rows, built on the
@@ -284,9 +288,10 @@ class SpatialProblem:
             return x_global.clone()
         return self.ops.tensor(np.asarray(x_global, dtype=np.float64)[self.lay.start: self.lay.stop])
 
-    def extend(self, x, slot="x"):
-        """x with its halos from the ring, in a persistent per-slot buffer."""
-        lay = self.lay
+    def extend(self, x, slot="x", lay=None):
+        """x with its halos (``lay``: the denoiser's by default) from the ring, in
+        a persistent per-slot buffer."""
+        lay = lay or self.lay
         ext = self._ext.get(slot)
         if ext is None:
             ext = self._ext[slot] = self.ops.zeros((lay.Hext, self.W))
@@ -302,8 +307,13 @@ class SpatialProblem:
         return self.comm.allreduce([self.ops.dot(a, b) for a, b in pairs])
 
     def matvec(self, p):
-        ext = self.extend(p, "p")
-        return self.interior(self.ops.normal_matvec(ext, self.lay.row0, self.H)).contiguous()
+        """(H^T H / sigma^2 + alpha I) p on the slab: p's halo is the operator's
+        reach (2r rows), so each CG iteration exchanges and recomputes 2r rows
+        per side, not the denoiser's (70 for PatchWeighted)."""
+        ol = self.op_lay
+        ext = self.extend(p, "p", ol)
+        q = self.ops.normal_matvec(ext, ol.row0, self.H)
+        return q[ol.halo: ol.halo + ol.rows].contiguous()
 
     # -- objective pieces (objective.py:78-121 on slabs)
     def denoise(self, x):
