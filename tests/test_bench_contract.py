@@ -30,11 +30,13 @@ def test_configs_cover_baseline(bench):
 
 def test_patch_weighted_bytes(bench):
     N = 1000
-    # (1 + 24 + 20 (24 + 2) + 27) N s with fp64 planes
-    assert bench.algorithmic_bytes("patch_weighted", 1, N) == 572 * N * 8
+    # the algorithm: x in, f out, the balancing field D in + out per sweep (20)
+    assert bench.algorithmic_bytes("patch_weighted", 1, N) == 42 * N * 8
+    assert bench.algorithmic_bytes("patch_weighted", 3, N, ws=4) == 3 * 42 * N * 8
+    # what the kernels stream: (1 + 24 + 20 (24 + 2) + 27) N s with fp64 planes
+    assert bench.pw_implementation_bytes(1, N) == 572 * N * 8
     # fp32 planes: N (8 + 24*4 + 20 (24*4 + 16) + 24*4 + 24) = 2464 N = 308 N s
-    assert bench.algorithmic_bytes("patch_weighted", 1, N, ws=4) == 308 * N * 8
-    assert bench.algorithmic_bytes("patch_weighted", 3, N, ws=4) == 3 * 308 * N * 8
+    assert bench.pw_implementation_bytes(1, N, ws=4) == 308 * N * 8
 
 
 def test_fourier_and_ve_bytes(bench):
