@@ -757,17 +757,34 @@ def run_native(a):
     x0_host = x0.cpu().pin_memory()
     x_host = torch.empty(x0.shape, dtype=torch.float64).pin_memory()
     e2e_steps = max(1, a.steps)
-    b2 = rv.RedBatch(op, ys_host, c["sigma"], ALPHA, den)  # warm the buffer cache
-    rv.solve_batch(b2, x0_host, cfg)
-    del b2
-    torch.cuda.synchronize()
+
+    def e2e_step(phases=None):
+        t_a = time.perf_counter()
+        b2 = rv.RedBatch(op, ys_host, c["sigma"], ALPHA, den)
+        t_b = time.perf_counter()
+        X, trs = rv.solve_batch(b2, x0_host, cfg)
+        t_c = time.perf_counter()
+        x_host.copy_(X)
+        torch.cuda.synchronize()
+        if phases is not None:
+            phases.append((t_b - t_a, t_c - t_b, time.perf_counter() - t_c))
+        del b2
+        return trs
+
+    # warm-up as for the device timing: W steps, then until two consecutive
+    # steps agree (buffer cache, graph capture, pinned staging, host allocator)
+    w_ms = []
+    for i in range(a.warmup + 20):
+        t_w = time.perf_counter()
+        e2e_step()
+        w_ms.append(1e3 * (time.perf_counter() - t_w))
+        if i + 1 >= a.warmup and len(w_ms) >= 2 and abs(w_ms[-1] - w_ms[-2]) <= 0.05 * w_ms[-2]:
+            break
     barrier()
+    phases = []
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        b2 = rv.RedBatch(op, ys_host, c["sigma"], ALPHA, den)
-        X, traces = rv.solve_batch(b2, x0_host, cfg)
-        x_host.copy_(X)
-        del b2
+        traces = e2e_step(phases)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_s = _reduce_max(torch.tensor([e2e_s], dtype=torch.float64, device="cuda"), world, shared)
@@ -794,7 +811,11 @@ def run_native(a):
                        "l2": "working set > L2 (ring of kappa+2 iterates per image)"
                        if B * N * 8 * (KAPPA + 2) > 126e6 else "working set fits L2"},
             "e2e": {"value": global_batch / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s,
+                    "warmup_ms": [round(v, 2) for v in w_ms],
+                    "phase_ms": {k: round(1e3 * statistics.median(v), 3) for k, v in
+                                 zip(("setup_h2d_y", "solve_h2d_x0_traces", "d2h_x"),
+                                     zip(*phases))}},
             "gpu_launches": int(launches),
             "settle_solves": settle,
             "methods": methods,

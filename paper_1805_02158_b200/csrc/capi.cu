@@ -259,9 +259,15 @@ struct redve_problem {
   DevBuf sp_m, sp_hh, sp_wr, sp_xb, sp_yh, sp_rh, sp_stage, sp_part, sp_cnt;
   bool sp_ready = false;
   cufftHandle sp_plan = 0, sp_plan1 = 0;  // batch B / batch 1, [H][W] complex
+  // CG fixed-point steps as graphs with a device-decided WHILE loop, keyed by
+  // their views / phase / f buffer
+  std::map<std::string, cudaGraphExec_t> cg_graphs;
+  cudaStream_t cg_body_stream = nullptr;
   ~redve_problem() {
     if (sp_plan) cufftDestroy(sp_plan);
     if (sp_plan1) cufftDestroy(sp_plan1);
+    for (auto& kv : cg_graphs) cudaGraphExecDestroy(kv.second);
+    if (cg_body_stream) cudaStreamDestroy(cg_body_stream);
   }
 
   int rd_nf = 0, rd_fs = 0;
@@ -406,6 +412,62 @@ static int cg_any_active(redve_problem* p, std::vector<CgState>& h) {
   return 0;
 }
 
+// The CG solve of one fixed-point step as a graph: init (pre-check), then a
+// WHILE node whose body is one CG iteration plus the device test "any image
+// still active" (k_cg_continue sets the loop condition), then the b == 0 and
+// maxiter residual epilogues.  No host round trip inside the solve.
+static int cg_graph_build(redve_problem* p, const CgArgs& a, const CgArgs& rres,
+                          cudaGraphExec_t* out) {
+  redve_ctx* ctx = p->ctx;
+  if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  if (!p->cg_body_stream) CK(cudaStreamCreateWithFlags(&p->cg_body_stream, cudaStreamNonBlocking));
+  const cudaStream_t cs = ctx->cap_stream, bs = p->cg_body_stream;
+  cudaGraph_t g = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  CK(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  launch_cg_init(a, cs);
+  launch_cg_continue(a, h, cs);
+  cudaStreamCaptureStatus st;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &nd);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode = nullptr;
+  if (e == cudaSuccess) e = cudaGraphAddNode(&cnode, g, deps, nd, &cp);
+  if (e == cudaSuccess)
+    e = cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies);
+  if (e == cudaSuccess) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      launch_cg_iter(a, bs);
+      launch_cg_update(a, bs);
+      launch_cg_continue(a, h, bs);
+      cudaGraph_t body_out = nullptr;
+      e = cudaStreamEndCapture(bs, &body_out);
+    }
+  }
+  launch_cg_zero_b(a, cs);
+  launch_cg_resid(rres, cs);
+  cudaGraph_t gout = nullptr;
+  const cudaError_t e2 = cudaStreamEndCapture(cs, &gout);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, REDVE_E_CUDA, "CG graph: %s", cudaGetErrorString(e));
+  }
+  return REDVE_OK;
+}
+
 // One CG fixed-point step (objective.py:105-121, scipy cg semantics) from xin
 // into xout; f_ext overrides the device denoiser (host plug-in).
 static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const double* f_ext) {
@@ -416,10 +478,11 @@ static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const do
     if (r) return r;
   }
   CgArgs a;
+  memset(&a, 0, sizeof(a));
   a.B = p->B; a.H = p->H; a.W = p->W; a.factor = p->op.factor; a.k = p->op.ksize;
   a.taps = p->htaps.as<double>();
   a.inv_sigma2 = 1.0 / (p->sigma * p->sigma); a.alpha = p->alpha;
-  a.rtol = 1e-6; a.abort = 1e-4; a.maxiter = 200; a.it = 0;  // objective.py:35-37
+  a.rtol = 1e-6; a.abort = 1e-4; a.maxiter = 200;  // objective.py:35-37
   a.row0 = 0; a.Hg = 0;
   a.huv = p->separable ? p->hsep.as<double>() : nullptr;
   a.xin = xin; a.xout = xout;
@@ -427,23 +490,40 @@ static int fp_step_cg(redve_problem* p, View xin, View xout, int phase, const do
   a.r = p->cr.as<double>(); a.p = p->cp.as<double>(); a.q = p->cq.as<double>();
   a.cg = p->cgst.as<CgState>(); a.st = p->state.as<ImgState>(); a.phase = phase;
   a.partials = p->part_cg.as<double>(); a.counters = p->cnt_cg.as<unsigned>();
+  CgArgs rres = a;
+  rres.xin = xout;
+  if (!ctx->profiling && graphs_enabled()) {
+    char key[256];
+    snprintf(key, sizeof(key), "%p|%lld|%lld|%d|%d|%p|%lld|%lld|%d|%d|%d|%p", (void*)xin.base,
+             xin.img_stride, xin.slot_stride, xin.S, xin.mode, (void*)xout.base,
+             xout.img_stride, xout.slot_stride, xout.S, xout.mode, phase, (const void*)a.f);
+    auto it = p->cg_graphs.find(key);
+    if (it == p->cg_graphs.end()) {
+      cudaGraphExec_t ge = nullptr;
+      int r = cg_graph_build(p, a, rres, &ge);
+      if (r) return r;
+      it = p->cg_graphs.emplace(key, ge).first;
+    }
+    CK(cudaGraphLaunch(it->second, s));
+    g_launches.fetch_add(4);  // init, continue, zero_b, resid (+3 per CG iteration)
+    return REDVE_OK;
+  }
+  // profiling: the same kernels launched one by one (per-kernel events), the
+  // loop test read back every 2 iterations
   RUN(ctx, "cg_init", launch_cg_init(a, s));
   CKL();
   std::vector<CgState> h;
   for (int it = 0; it < a.maxiter; ++it) {
-    if (it % 2 == 0) {  // host check of the per-image stop flags every 2 iterations
+    if (it % 2 == 0) {
       int any = cg_any_active(p, h);
       if (any > 1) return any;
       if (!any) break;
     }
-    a.it = it;
     RUN(ctx, "cg_matvec", launch_cg_iter(a, s));
     RUN(ctx, "cg_update", launch_cg_update(a, s));
     CKL();
   }
   RUN(ctx, "cg_zero_b", launch_cg_zero_b(a, s));
-  CgArgs rres = a;
-  rres.xin = xout;
   RUN(ctx, "cg_resid", launch_cg_resid(rres, s));
   CKL();
   return REDVE_OK;

@@ -602,7 +602,8 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
   for (int i = threadIdx.x; i < k * k; i += blockDim.x) taps[i] = a.taps[i];
   const long long N = (long long)H * W;
   const int i0 = blockIdx.y * MV_TH, j0 = blockIdx.x * MV_TW;
-  const double beta = (MODE == CG_ITER && a.it > 0) ? cs.beta : 0.0;
+  const bool cont = MODE == CG_ITER && cs.its > 0;  // p = r + beta p_old after the 1st iteration
+  const double beta = cont ? cs.beta : 0.0;
   const double* rr = a.r + (long long)b * N;
   const double* pold = a.p + (long long)b * N;
   const double* xin = (MODE == CG_ITER) ? nullptr : a.xin.at(b, a.st);
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(256) k_cg_matvec(CgArgs a) {
     const long long o =
         (long long)wrap_fast(i0 - 2 * r + ti, H) * W + wrap_fast(j0 - 2 * r + tj, W);
     double w;
-    if (MODE == CG_ITER) w = (a.it > 0) ? fma(beta, pold[o], rr[o]) : rr[o];
+    if (MODE == CG_ITER) w = cont ? fma(beta, pold[o], rr[o]) : rr[o];
     else w = xin[o];
     ws[idx] = w;
   }
@@ -786,8 +787,8 @@ __device__ __forceinline__ bool mvp_vec_ok(const CgArgs& a, int j0) {
 // loads issued before its shared-memory stores (the load is the exposed latency)
 template <int MODE>
 __device__ __forceinline__ void mvp_load(const CgArgs& a, const double* src_x, const double* rr,
-                                         const double* pold, double beta, int i0, int j0,
-                                         double* ws) {
+                                         const double* pold, bool cont, double beta, int i0,
+                                         int j0, double* ws) {
   using G = MvpGeom;
   constexpr int R = G::R, HX = G::HX, WX = G::WX;
   const int H = a.H, W = a.W;
@@ -803,7 +804,7 @@ __device__ __forceinline__ void mvp_load(const CgArgs& a, const double* src_x, c
         const long long o = (long long)wrap_near(i0 - 2 * R + ti, H) * W + j0 - 2 * R + 2 * c2;
         if (MODE == CG_ITER) {
           const double2 rv = *reinterpret_cast<const double2*>(rr + o);
-          if (a.it > 0) {
+          if (cont) {
             const double2 pv = *reinterpret_cast<const double2*>(pold + o);
             v[q] = make_double2(fma(beta, pv.x, rv.x), fma(beta, pv.y, rv.y));
           } else {
@@ -826,7 +827,7 @@ __device__ __forceinline__ void mvp_load(const CgArgs& a, const double* src_x, c
       for (int tj = lane; tj < WX; tj += 32) {
         const long long o = ro + wrap_fast(j0 - 2 * R + tj, W);
         double w;
-        if (MODE == CG_ITER) w = (a.it > 0) ? fma(beta, pold[o], rr[o]) : rr[o];
+        if (MODE == CG_ITER) w = cont ? fma(beta, pold[o], rr[o]) : rr[o];
         else w = src_x[o];
         ws[ti * WX + tj] = w;
       }
@@ -1110,9 +1111,10 @@ __global__ void __launch_bounds__(256, 4) k_cg_matvec_ct(CgArgs a) {
   const int H = a.H, W = a.W;
   const long long N = (long long)H * W;
   const int i0 = a.tile_off + (blockIdx.y - 1) * TH, j0 = blockIdx.x * TW;
-  const double beta = (MODE == CG_ITER && a.it > 0) ? cs.beta : 0.0;
+  const bool cont = MODE == CG_ITER && cs.its > 0;  // p = r + beta p_old after the 1st iteration
+  const double beta = cont ? cs.beta : 0.0;
   const double* xin = (MODE == CG_ITER) ? nullptr : a.xin.at(b, a.st);
-  mvp_load<MODE>(a, xin, a.r + (long long)b * N, a.p + (long long)b * N, beta, i0, j0, ws);
+  mvp_load<MODE>(a, xin, a.r + (long long)b * N, a.p + (long long)b * N, cont, beta, i0, j0, ws);
   const bool regular = mvp_lattice(a, i0, j0, m);  // its barrier also completes ws
   double acc[2] = {0.0, 0.0};
   const double inv_s2 = a.inv_sigma2;
@@ -1219,6 +1221,18 @@ __global__ void k_cg_zero_b(CgArgs a) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
        i += (long long)gridDim.x * blockDim.x)
     x[i] = 0.0;
+}
+
+// WHILE-node condition of the CG loop: another iteration while any image's
+// CG is active (scipy's loop test, iterative.py:406, decided on the device)
+__global__ void k_cg_continue(const CgState* cg, int B, cudaGraphConditionalHandle h) {
+  int any = 0;
+  for (int b = threadIdx.x; b < B; b += 32) any |= cg[b].active;
+  any = __any_sync(0xffffffffu, any);
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, any ? 1u : 0u);
+}
+void launch_cg_continue(const CgArgs& a, cudaGraphConditionalHandle h, cudaStream_t s) {
+  k_cg_continue<<<1, 32, 0, s>>>(a.cg, a.B, h);
 }
 
 size_t cg_matvec_smem(int k) {

@@ -32,7 +32,7 @@ struct CgArgs {
   const double* taps;  // device k*k
   const double* huv;   // rank-one PSF: device [u | v] (k each), else null
   double inv_sigma2, alpha, rtol, abort;
-  int maxiter, it;
+  int maxiter;
   int row0, Hg;        // global row of local row 0 / global height (0: the buffer is the image)
   int tile_off;        // compile-time operator kernel: local row of a lattice-aligned tile origin,
   int row0m, seam;     // row0 mod Hg, local row of global row 0 (-1: none)  (set by the launcher)
@@ -71,6 +71,7 @@ void launch_cg_iter(const CgArgs& a, cudaStream_t s);
 void launch_cg_resid(const CgArgs& a, cudaStream_t s);
 void launch_normal_matvec(const CgArgs& a, cudaStream_t s);  // q = A w, every row
 void launch_cg_update(const CgArgs& a, cudaStream_t s);
+void launch_cg_continue(const CgArgs& a, cudaGraphConditionalHandle h, cudaStream_t s);
 void launch_cg_zero_b(const CgArgs& a, cudaStream_t s);
 void launch_step_record(const RecordArgs& a, int B, cudaStream_t s);
 void launch_denoise_view(View xin, DenoiseArgs dn, double* out, const ImgState* st, int phase,

@@ -193,3 +193,31 @@ def test_config3_512_filter_bank_vs_reference_drivers(rv, golden):
     for s in (0, 1):
         assert rel(X[s], g[f"s{s}/mpe/x32"]) <= 1e-5
         cmp_trace(traces[s], g, f"s{s}/mpe")
+
+
+# ----------------------------------------------------------------- CG route graphs
+@pytest.mark.parametrize("method", ["fp", "fp-ve"])
+def test_cg_graph_equals_host_driven_loop(rv, monkeypatch, method):
+    """The CG solve of every fixed-point step runs as a graph whose WHILE node
+    the device ends (k_cg_continue); REDVE_GRAPHS=0 drives the same kernels
+    from the host, reading the stop flags back every 2 iterations.  Same
+    kernels, same order: identical iterates and CG iteration counts."""
+    from oracle import redve_ref as R
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    truths = np.stack([voronoi_scene(s, 96) for s in range(3)])
+    op_o = R.BlurDecimate(R.psf_taps("gaussian", 7, 1.6), 3, (96, 96))
+    ys = np.stack([R.measure(truths[b], op_o, 5.0, b) for b in range(3)])
+    op = rv.BlurDownsample(rv.make_psf("gaussian", 7, 1.6), 3, (96, 96))
+    x0 = np.stack([op_o.adjoint(y) for y in ys])
+    cfg = rv.SolveConfig(method=method, ve_method="rre", max_inner_steps=12)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("REDVE_GRAPHS", flag)
+        batch = rv.RedBatch(op, ys, 5.0, 0.02, rv.GaussianFilter(), truths)
+        res = batch.solve(x0, cfg)
+        out[flag] = (res.x.cpu().numpy(), res.cg_iters.copy(), res.n_records.copy())
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][1], out["0"][1])
+    np.testing.assert_array_equal(out["1"][2], out["0"][2])
+    assert out["1"][1].max() >= 2  # the WHILE loop ran several iterations
