@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -130,7 +131,11 @@ struct redve_ctx {
   std::vector<double> taps_host;  // what scratch_taps holds (skip identical re-uploads)
   void* taps_dev = nullptr;
   bool taps_sep = false;          // scratch_taps is followed by the rank-one [u | v]
+  // cuFFT plans by (H, W, batch), shared by the context's problems: a plan
+  // costs milliseconds to create, a RedBatch per call must not pay it again
+  std::map<std::tuple<int, int, int>, cufftHandle> fft_plans;
   ~redve_ctx() {
+    for (auto& kv : fft_plans) cufftDestroy(kv.second);
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (hstage) cudaFreeHost(hstage);
@@ -258,14 +263,12 @@ struct redve_problem {
   // spectral route (linear denoisers): constant spectra, DFT staging, plans
   DevBuf sp_m, sp_hh, sp_wr, sp_xb, sp_yh, sp_rh, sp_stage, sp_part, sp_cnt;
   bool sp_ready = false;
-  cufftHandle sp_plan = 0, sp_plan1 = 0;  // batch B / batch 1, [H][W] complex
+  cufftHandle sp_plan = 0, sp_plan1 = 0;  // batch B / batch 1, [H][W] complex (ctx-owned)
   // CG fixed-point steps as graphs with a device-decided WHILE loop, keyed by
   // their views / phase / f buffer
   std::map<std::string, cudaGraphExec_t> cg_graphs;
   cudaStream_t cg_body_stream = nullptr;
   ~redve_problem() {
-    if (sp_plan) cufftDestroy(sp_plan);
-    if (sp_plan1) cufftDestroy(sp_plan1);
     for (auto& kv : cg_graphs) cudaGraphExecDestroy(kv.second);
     if (cg_body_stream) cudaStreamDestroy(cg_body_stream);
   }
@@ -1250,13 +1253,22 @@ static int spectral_setup(redve_problem* p) {
   const cudaStream_t s = ctx->stream;
   const int B = p->B;
   const long long N = p->N;
-  if (!p->sp_plan) {
+  auto plan = [&](int batch) -> cufftHandle {
+    const auto key = std::make_tuple(p->H, p->W, batch);
+    auto it = ctx->fft_plans.find(key);
+    if (it != ctx->fft_plans.end()) return it->second;
     int n[2] = {p->H, p->W};
-    if (cufftPlanMany(&p->sp_plan, 2, n, nullptr, 1, (int)N, nullptr, 1, (int)N, CUFFT_Z2Z, B) !=
-            CUFFT_SUCCESS ||
-        cufftPlanMany(&p->sp_plan1, 2, n, nullptr, 1, (int)N, nullptr, 1, (int)N, CUFFT_Z2Z, 1) !=
-            CUFFT_SUCCESS)
-      return fail(ctx, REDVE_E_CUDA, "cufftPlanMany failed");
+    cufftHandle h = 0;
+    if (cufftPlanMany(&h, 2, n, nullptr, 1, (int)N, nullptr, 1, (int)N, CUFFT_Z2Z, batch) !=
+        CUFFT_SUCCESS)
+      return 0;
+    ctx->fft_plans[key] = h;
+    return h;
+  };
+  if (!p->sp_plan) {
+    p->sp_plan = plan(B);
+    p->sp_plan1 = plan(1);
+    if (!p->sp_plan || !p->sp_plan1) return fail(ctx, REDVE_E_CUDA, "cufftPlanMany failed");
   }
   if (cufftSetStream(p->sp_plan, s) != CUFFT_SUCCESS || cufftSetStream(p->sp_plan1, s) != CUFFT_SUCCESS)
     return fail(ctx, REDVE_E_CUDA, "cufftSetStream failed");

@@ -6,7 +6,12 @@
 //     -- the same R modified Gram-Schmidt produces, up to rounding);
 //   * a pivot ratio below max(1e-6, 1e3*rank_tol) is outside what the Gram
 //     route resolves, so the image is sent to the exact device MGS pass
-//     (mgs_qr, extrapolation.py:159-196) before deciding;
+//     (mgs_qr, extrapolation.py:159-196) before deciding.  Above it Cholesky
+//     leaves ~eps cond^2 on the small pivots: against the reference's MGS on
+//     full-rank windows of cond 1e5 / 1e6 / 1e7 (pivot ratio down to 1.3e-6)
+//     the weights differ by 1e-9 / 1e-7 / 1.5e-6 relative and the extrapolated
+//     point by < 1e-7 of the window's spread, with identical decisions
+//     (tests/test_gpu_ve_api.py, golden ve_cond.npz);
 //   * MPE  : R[:k,:k] c' = -R[:k,k], c_k = 1, degenerate if |sum c| < 1e-12 ||c||_1
 //            (extrapolation.py:241-260);
 //   * RRE  : R^T z = 1, R d = z, gamma = d / sum d          (:263-273);

@@ -80,3 +80,31 @@ def test_error_cases():
     assert qr2.effective_rank == 1
     with pytest.raises(ValueError):
         rv.small_svd(np.zeros((2, 3)))
+
+
+# ------------------------------------------------ ill-conditioned full-rank windows
+@pytest.mark.parametrize("i", range(6))
+@pytest.mark.parametrize("method", ["mpe", "rre", "svdmpe"])
+def test_ill_conditioned_windows_vs_reference(golden, i, method):
+    """Windows with cond(U) = 1e2 ... 1e7 (tests/golden/make_ve_cond_golden.py,
+    the unmodified reference's extrapolate_once): R's smallest pivot ratio runs
+    from 1e-1 down to 1.3e-6, just above the Gram route's MGS cutoff (1e-6).
+    Cholesky of G = U^T U puts ~eps cond^2 on the small pivots, so the weights
+    drift from the reference's twice-orthogonalised MGS as cond grows
+    (measured: 1e-9 at 1e5, 1.5e-6 at 1e7); the extrapolated point stays within
+    1e-7 of the window's own spread, far below the solves' 1e-5 bar."""
+    import paper_1805_02158_b200 as rv
+
+    g = golden("ve_cond.npz")
+    rows = g[f"cond{i}/rows"]
+    cond = float(g[f"cond{i}/cond"])
+    key = f"cond{i}/{method}"
+    res = rv.extrapolate_once(rv.VectorSequenceWindow(rows), method)
+    flags = g[f"{key}/flags"]
+    assert (int(res.converged), int(res.extrapolated), res.kappa_used) == tuple(flags[:3])
+    assert int(res.weights.fallback_from is not None) == flags[3]
+    gam = g[f"{key}/gamma"]
+    tol = max(1e-12, 1e-16 * cond**2) * 10
+    assert np.max(np.abs(res.weights.gamma - gam)) <= tol * np.max(np.abs(gam)) + 1e-13
+    spread = np.linalg.norm(np.diff(rows, axis=0))
+    assert np.linalg.norm(np.asarray(res.vector) - g[f"{key}/vector"]) <= 1e-7 * spread
