@@ -649,6 +649,17 @@ static int put_taps(redve_ctx* ctx, const double* taps, int k) {
   return REDVE_OK;
 }
 
+// ctx->scratch_taps (k x k) through the rank-one two-pass stencil when the
+// taps split, else the 2-D stencil kernels
+static void conv_scratch(redve_ctx* ctx, const double* x, double* out, int B, int H, int W, int k,
+                         int corr) {
+  const double* taps = ctx->scratch_taps.as<double>();
+  if (ctx->taps_sep &&
+      launch_conv_rank1(x, out, B, H, W, taps + (size_t)k * k, k, corr, 1.0, ctx->stream))
+    return;
+  launch_conv(x, out, B, H, W, taps, k, corr, 1.0, ctx->stream);
+}
+
 // ------------------------------------------------------------------ denoise
 int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, int W,
                   const double* x, double* out) {
@@ -669,7 +680,7 @@ int redve_denoise(redve_ctx* ctx, const redve_denoiser_desc* dn, int B, int H, i
         return fail(ctx, REDVE_E_KERNEL, "%dx%d PSF on a %dx%d image", dn->ksize, dn->ksize, H, W);
       int rc = put_taps(ctx, dn->taps, dn->ksize);
       if (rc) return rc;
-      RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), dn->ksize, 0, 1.0, ctx->stream));
+      RUN(ctx, "conv", conv_scratch(ctx, x, out, B, H, W, dn->ksize, 0));
       CKL();
       // taps buffer is reused by the next call: keep it alive until then
       CK(cudaStreamSynchronize(ctx->stream));
@@ -784,7 +795,7 @@ int redve_operator_apply(redve_ctx* ctx, const redve_operator_desc* op, int B, i
   if (x == out) return fail(ctx, REDVE_E_VALUE, "out must not alias x");
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
-    RUN(ctx, "conv", launch_conv(x, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 0, 1.0, ctx->stream));
+    RUN(ctx, "conv", conv_scratch(ctx, x, out, B, H, W, op->ksize, 0));
   } else {
     RUN(ctx, "decimate_conv", launch_decimate_conv(x, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
                          ctx->stream));
@@ -801,7 +812,7 @@ int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B,
   if (z == out) return fail(ctx, REDVE_E_VALUE, "out must not alias z");
   if ((rc = upload_taps(ctx, op))) return rc;
   if (op->kind == REDVE_OP_BLUR) {
-    RUN(ctx, "conv", launch_conv(z, out, B, H, W, ctx->scratch_taps.as<double>(), op->ksize, 1, 1.0, ctx->stream));
+    RUN(ctx, "conv", conv_scratch(ctx, z, out, B, H, W, op->ksize, 1));
   } else {
     RUN(ctx, "upsample_corr", launch_upsample_corr(z, out, B, H, W, op->factor, ctx->scratch_taps.as<double>(), op->ksize,
                          1.0, ctx->stream));
@@ -1010,9 +1021,16 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     RUN(ctx, "upsample_corr", launch_upsample_corr(p->y.as<double>(), p->hty.as<double>(), B, H, W,
                                                    op->factor, p->htaps.as<double>(), op->ksize,
                                                    1.0 / (sigma * sigma), s));
-  } else
-  RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W, p->htaps.as<double>(),
-              op->ksize, 1, 1.0 / (sigma * sigma), s));
+  } else {  // rank-one PSFs as two 1-D passes
+    bool done = false;
+    if (p->separable)
+      RUN(ctx, "conv", done = launch_conv_rank1(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                                p->hsep.as<double>(), op->ksize, 1,
+                                                1.0 / (sigma * sigma), s));
+    if (!done)
+      RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                   p->htaps.as<double>(), op->ksize, 1, 1.0 / (sigma * sigma), s));
+  }
   PK(cudaGetLastError());
   if (p->fourier) {
     p->twH = ctx->tw(H);

@@ -1023,6 +1023,73 @@ static bool launch_stencil8(const double* x, double* out, int B, int H, int W, c
   }
 }
 
+// Rank-one K x K stencil (taps = u v^T: the uniform and Gaussian PSFs) as two
+// 1-D passes over a shared-memory tile: 2K FMAs per output instead of K^2 and
+// every input read once from HBM.  out = scale * (conv or corr)(x), periodic.
+// The terms are regrouped: equal to the 2-D sum to rounding.
+constexpr int SEP_TH = 32, SEP_TW = 64;
+
+template <int K, int CORR>
+__global__ void __launch_bounds__(256) k_sep_stencil(const double* x, double* out, int H, int W,
+                                                     const double* uv, double scale) {
+  constexpr int XW = SEP_TW + K - 1, XH = SEP_TH + K - 1, R = K / 2;
+  __shared__ double xs[XH][XW];
+  __shared__ double hs[XH][SEP_TW];
+  const int b = blockIdx.z;
+  const long long N = (long long)H * W;
+  const double* xb = x + (long long)b * N;
+  const int i0 = blockIdx.y * SEP_TH, j0 = blockIdx.x * SEP_TW;
+  for (int idx = threadIdx.x; idx < XH * XW; idx += blockDim.x) {
+    const int r = idx / XW, c = idx - r * XW;
+    xs[r][c] = __ldg(xb + (long long)wrap_fast(i0 - R + r, H) * W + wrap_fast(j0 - R + c, W));
+  }
+  double u[K], v[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    u[t] = __ldg(uv + t);
+    v[t] = __ldg(uv + K + t);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < XH * SEP_TW; idx += blockDim.x) {
+    const int r = idx / SEP_TW, c = idx - r * SEP_TW;
+    double h = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) h = fma(v[t], xs[r][CORR ? c + t : c + K - 1 - t], h);
+    hs[r][c] = h;
+  }
+  __syncthreads();
+  double* ob = out + (long long)b * N;
+  for (int idx = threadIdx.x; idx < SEP_TH * SEP_TW; idx += blockDim.x) {
+    const int r = idx / SEP_TW, c = idx - r * SEP_TW;
+    const int gi = i0 + r, gj = j0 + c;
+    if (gi >= H || gj >= W) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) acc = fma(u[t], hs[CORR ? r + t : r + K - 1 - t][c], acc);
+    ob[(long long)gi * W + gj] = scale * acc;
+  }
+}
+
+template <int K>
+static void sep_k(const double* x, double* out, int B, int H, int W, const double* uv, int corr,
+                  double scale, cudaStream_t s) {
+  const dim3 grid(cdiv(W, SEP_TW), cdiv(H, SEP_TH), B);
+  if (corr) k_sep_stencil<K, 1><<<grid, 256, 0, s>>>(x, out, H, W, uv, scale);
+  else k_sep_stencil<K, 0><<<grid, 256, 0, s>>>(x, out, H, W, uv, scale);
+}
+
+bool launch_conv_rank1(const double* x, double* out, int B, int H, int W, const double* uv, int k,
+                       int corr, double scale, cudaStream_t s) {
+  if (H < k || W < k) return false;
+  switch (k) {
+    case 3: sep_k<3>(x, out, B, H, W, uv, corr, scale, s); return true;
+    case 5: sep_k<5>(x, out, B, H, W, uv, corr, scale, s); return true;
+    case 7: sep_k<7>(x, out, B, H, W, uv, corr, scale, s); return true;
+    case 9: sep_k<9>(x, out, B, H, W, uv, corr, scale, s); return true;
+    default: return false;
+  }
+}
+
 // --------------------------------------------------------------- stencils (operator API)
 // out = scale * (conv or corr)(x, taps), periodic   (imaging.py:132-170)
 __global__ void k_conv(const double* x, double* out, int B, int H, int W, const double* taps,

@@ -175,6 +175,9 @@ void launch_gather(double* out, View cur, const double* best, int B, long long N
                    const ImgState* st, cudaStream_t s);
 void launch_conv(const double* x, double* out, int B, int H, int W, const double* taps, int k,
                  int corr, double scale, cudaStream_t s);
+// rank-one taps (uv = [u | v]): two 1-D passes; false if k is not compiled
+bool launch_conv_rank1(const double* x, double* out, int B, int H, int W, const double* uv, int k,
+                       int corr, double scale, cudaStream_t s);
 void launch_decimate_conv(const double* x, double* out, int B, int H, int W, int factor,
                           const double* taps, int k, cudaStream_t s);
 void launch_upsample_corr(const double* z, double* out, int B, int H, int W, int factor,
