@@ -323,6 +323,10 @@ def run_reference(a):
         return
     solve_fn = _ref_solve if kind == "reference" else _oracle_solve
     nb = a.batch or c["batch"]
+    # the native arm's workload at --gpus N: N batches of nb (weak scaling) or
+    # one batch of nb split across the ranks (strong); each timed step here
+    # solves nb of those images (a bounded sample; the rate is per image)
+    global_batch = nb * a.gpus if c["scaling"] == "weak" else nb
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(cores, initializer=_single_thread_env) as pool:
@@ -338,7 +342,9 @@ def run_reference(a):
                     times.append(time.perf_counter() - t0)
             ms = 1e3 * statistics.mean(times)
             value = nb / (ms / 1e3)
-            sample = f"all {nb} images x {BUDGET} iterations per step, process pool of {cores}"
+            sample = (f"{nb} of the {global_batch} images x {BUDGET} iterations per step, "
+                      f"process pool of {cores}" if global_batch != nb else
+                      f"all {nb} images x {BUDGET} iterations per step, process pool of {cores}")
         else:
             # large images: a bounded sample of fixed-point iterations, one image per
             # core, scaled to solves/s at BUDGET iterations per solve
@@ -359,7 +365,7 @@ def run_reference(a):
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": c["workload"], "sample": sample,
-                                        "global_batch": nb},
+                                        "global_batch": global_batch},
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": kind,
                          "sample": who + sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
@@ -868,7 +874,7 @@ def run_spatial(a):
     x0 = np.asarray(op.adjoint(y))            # zero-filled adjoint initialisation
     del clean
     den = product_denoiser(c)
-    comm = TorchComm(device="cuda")
+    comm = TorchComm(device="cpu" if shared else "cuda")  # gloo carries host tensors
     prob = SpatialProblem(op, y, c["sigma"], ALPHA, den, comm=comm, reference=truth)
     cfg = rv.SolveConfig(method="fp-ve", ve_method="rre", m=0, kappa=KAPPA,
                          max_inner_steps=SPATIAL_BUDGET)
