@@ -1497,7 +1497,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     // normal-equation identity (k_cost_fp) with f(x_{k-1}) kept by k_row_fwd
     // (fused denoisers) or by the step itself (precomputed denoisers).  For the
     // precomputed denoisers f(x_k) evaluated here is handed to the next step
-    // when nothing changes the iterate in between (f_ready).
+    // when nothing changes the iterate in between (f_ready); the CG route
+    // reuses it the same way.
     const bool ident = p->fourier && !gradm;  // the cost identity holds for FP steps only
     double* f_step = p->fbuf.as<double>();   // f of the current step's input
     double* f_spare = p->fcur.as<double>();  // f of the new iterate (cost)
@@ -1535,6 +1536,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       if (pw && ident && mode != COST_FINAL) {  // f(cur) is ready for the next step
         std::swap(f_step, f_spare);
         f_ready = true;
+      } else if (pw && !p->fourier && !gradm && mode != COST_FINAL) {
+        f_ready = true;  // CG route: f(cur) sits in fbuf, where the next step reads it
       }
       return REDVE_OK;
     };
@@ -1631,7 +1634,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
         if ((r = f_col(p, zcur, p->alpha, phase))) return r;
         r = f_row_inv(p, zcur, nxt, p->xb.as<double>(), 1, cur, c, tr, S);
       } else {
-        r = fp_step_cg(p, cur, nxt, phase, nullptr);
+        // a cadence cost already denoised cur into fbuf (PatchWeighted: ~30%
+        // of a configs[2] solve): the CG step takes it as its f
+        r = fp_step_cg(p, cur, nxt, phase, f_ready ? p->fbuf.as<double>() : nullptr);
+        f_ready = false;
         if (r) return r;
         RecordArgs ra;
         ra.cg = p->cgst.as<CgState>();
