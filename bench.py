@@ -774,7 +774,10 @@ def run_native(a):
     # problem setup from the host measurements, H2D of y and x0, the solve, D2H of
     # the solutions (traces come back inside solve_batch)
     ys_host = torch.from_numpy(ys).pin_memory()
-    x0_host = x0.cpu().pin_memory()
+    # deblurring starts from x0 = y (cli.py:362-363): the user hands the same
+    # array, which RedBatch already uploaded; SR starts from the adjoint
+    x0_is_y = c["kind"] != "sr"
+    x0_host = ys_host if x0_is_y else x0.cpu().pin_memory()
     x_host = torch.empty(x0.shape, dtype=torch.float64).pin_memory()
     e2e_steps = max(1, a.steps)
 
@@ -809,7 +812,7 @@ def run_native(a):
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_s = _reduce_max(torch.tensor([e2e_s], dtype=torch.float64, device="cuda"), world, shared)
     assert len(traces) == B
-    h2d = ys.nbytes + x0.numel() * 8          # measurements for the problem + x0
+    h2d = ys.nbytes + (0 if x0_is_y else x0.numel() * 8)  # measurements (+ x0 for SR)
     d2h = x0.numel() * 8 + B * (BUDGET * 5 * 8)  # solutions + per-record trace arrays
 
     cpu = None

@@ -60,6 +60,7 @@ class RedBatch:
         self.B = int(yt.shape[0])
         self.shape = tuple(forward.in_shape)
         self.y = yt.contiguous()
+        self._y_src = ys  # x0 = y (the deblurring default, cli.py:362-363) reuses self.y
         self.ref = None
         if references is not None:
             rt, _ = _io.to_device(references)
@@ -164,7 +165,10 @@ class RedBatch:
         gradient = method in ("sd", "sd-ve", "nesterov")
         if gradient and (config.step_size is None or config.step_size <= 0):
             raise ValueError("this method needs a positive step_size")
-        t, from_np, _ = self._batch_in(x0)  # finiteness of x0: checked on the device
+        if x0 is self._y_src and tuple(self.y.shape[1:]) == self.shape:
+            t = self.y  # the measurements already on the device: no second upload
+        else:
+            t, _, _ = self._batch_in(x0)  # finiteness of x0: checked on the device
         cfg = nat.SolveConfigC()
         cfg.method = nat.METHOD_CODES[method]
         cfg.ve_method = nat.VE_CODES[config.ve_method]

@@ -221,3 +221,20 @@ def test_cg_graph_equals_host_driven_loop(rv, monkeypatch, method):
     np.testing.assert_array_equal(out["1"][1], out["0"][1])
     np.testing.assert_array_equal(out["1"][2], out["0"][2])
     assert out["1"][1].max() >= 2  # the WHILE loop ran several iterations
+
+
+def test_x0_is_y_reuses_the_device_measurements(rv):
+    """x0 handed as the very array the batch was built from (x0 = y, the
+    deblurring default) skips the second upload; the solve is unchanged."""
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    n = 64
+    op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
+    truths = np.stack([voronoi_scene(s, n) for s in range(3)])
+    clean = np.asarray(op.apply(truths))
+    ys = np.stack([clean[i] + rv.gaussian_noise((n, n), SQRT2, i) for i in range(3)])
+    cfg = rv.SolveConfig(method="fp-ve", max_inner_steps=12)
+    batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.Median3())
+    a = batch.solve(ys, cfg).x.cpu().numpy()
+    b = batch.solve(ys.copy(), cfg).x.cpu().numpy()
+    np.testing.assert_array_equal(a, b)
