@@ -1235,7 +1235,13 @@ static int ve_chunks(int B, long long N) {
     const int c = atoi(e);
     if (c >= 1 && c <= 64) return c;
   }
-  const long long resident = 2LL * 148;
+  static long long resident = 0;  // 2 CTAs per SM (k_gram / k_combine at 128 registers)
+  if (resident == 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = 2LL * (sms > 0 ? sms : 148);
+  }
   int best = 1;
   double best_cost = 1e300;
   for (int c = 1; c <= 64; ++c) {
