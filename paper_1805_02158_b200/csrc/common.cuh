@@ -66,11 +66,13 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem_red /* >
 // "Last block done" handshake: every block of a group publishes partials, then
 // the block that arrives last (per group) sees all of them.  Returns true in
 // the last block.  Counter is reset by the last block, so it can be reused.
+// Thread 0 writes its block's partials, so thread 0 alone fences them before
+// counting: the other threads' outputs (only read by later kernels) are not
+// waited for -- a block-wide fence stalled every thread on its own stores.
 __device__ __forceinline__ bool last_block_of_group(unsigned int* counter, unsigned int nblocks,
                                                     int* smem_flag) {
-  __threadfence();
-  __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     unsigned int prev = atomicAdd(counter, 1u);
     int last = (prev == nblocks - 1);
     if (last) *counter = 0u;
