@@ -66,6 +66,14 @@ struct View {
   long long slot_stride;  // elements between ring slots (0 for plain)
   int S;                  // ring length (1 for plain)
   int mode;               // 0 plain, 1 current slot, 2 next slot, 3 cycle start slot
+  // as at(), from a copy of image b's state
+  __device__ __forceinline__ double* at_state(int b, const ImgState& s) const {
+    double* p = base + (long long)b * img_stride;
+    if (mode == 1) p += (long long)s.cur * slot_stride;
+    else if (mode == 2) p += (long long)((s.cur + 1) % S) * slot_stride;
+    else if (mode == 3) p += (long long)s.start * slot_stride;
+    return p;
+  }
   __device__ __forceinline__ double* at(int b, const ImgState* st) const {
     double* p = base + (long long)b * img_stride;
     if (mode == 1) p += (long long)st[b].cur * slot_stride;

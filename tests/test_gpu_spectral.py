@@ -109,3 +109,32 @@ def test_spectral_graph_reuse_and_nonfinite(rv):
     bad[0, 0, 0] = np.inf
     with pytest.raises(ValueError, match="non-finite"):
         batch.solve(bad, cfg)
+
+
+@pytest.mark.parametrize("B,n", [(1, 256), (3, 64), (2, 128)])
+@pytest.mark.parametrize("method,stab", [("fp", 0), ("fp-ve", 0), ("fp-ve", 3)])
+def test_fused_cluster_steps_equal_per_step_kernels(rv, monkeypatch, B, n, method, stab):
+    """Small batches run the spectral steps of a cycle in one cluster launch
+    (k_spec_steps); REDVE_SPEC_FUSED=0 launches k_spec_step per step.  The
+    step arithmetic is the same, so the iterates agree bit for bit; the
+    recorded sums are reduced over DSMEM in another fixed order (1e-13)."""
+    from paper_1805_02158_b200.synth import voronoi_scene
+
+    op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
+    truths = np.stack([voronoi_scene(s, n) for s in range(B)])
+    clean = np.asarray(op.apply(truths))
+    ys = np.stack([clean[i] + rv.gaussian_noise((n, n), SQRT2, i) for i in range(B)])
+    cfg = rv.SolveConfig(method=method, max_inner_steps=40, stabilization_iters=stab)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("REDVE_SPEC_FUSED", flag)
+        batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.GaussianFilter(), truths)
+        res = batch.solve(ys, cfg)
+        out[flag] = res
+    a, b = out["1"], out["0"]
+    np.testing.assert_array_equal(a.x.cpu().numpy(), b.x.cpu().numpy())
+    np.testing.assert_array_equal(a.n_records, b.n_records)
+    np.testing.assert_allclose(a.step_norm, b.step_norm, rtol=1e-12, equal_nan=True)
+    np.testing.assert_allclose(a.cost, b.cost, rtol=1e-12, equal_nan=True)
+    np.testing.assert_allclose(a.psnr, b.psnr, rtol=1e-12, equal_nan=True)
+    np.testing.assert_array_equal(a.n_cycles, b.n_cycles)
