@@ -1448,7 +1448,7 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
   char topo[512], keybuf[640];
   snprintf(topo, sizeof(topo), "%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%d|%.17g|%d|%.17g|%.17g",
            p->B, p->H, p->W, p->op.kind, p->op.ksize, p->dn_api_kind, p->dn_ksize, (int)pw,
-           (int)spec + (spec && spec_steps_fits(p->B, p->N) ? 2 : 0),
+           (int)spec + (spec && spec_run_fits(p->B, p->N, ve ? kp1 : 2) ? 2 : 0),
            cfg->method, cfg->ve_method, cfg->m, cfg->kappa, cfg->max_inner_steps, cfg->tol,
            cfg->stabilization_iters, cfg->rank_tolerance, gradm ? cfg->step_size : 0.0);
   snprintf(keybuf, sizeof(keybuf), "%s|%llu|%p|%p|%p|%p", topo, p->serial, p->ring.p, p->trace.p,
@@ -1666,13 +1666,11 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       return REDVE_OK;
     };
 
-    // spectral route, small batches: n consecutive steps in one cluster launch
-    // (k_spec_steps); step i records the cost when the unfused schedule would
-    const bool spec_fused = spec && spec_steps_fits(B, N);
-    auto spec_steps = [&](int phase, int n, int kstart, bool all_cadence) -> int {
-      unsigned mask = 0;
-      for (int i = 0; i < n; ++i)
-        if (all_cadence || ((kstart + i + 1) % log_every) == 0) mask |= 1u << i;
+    // spectral route, small batches: the whole schedule below (steps, cadence
+    // costs, best copies, VE after every full cycle) as one cluster launch per
+    // image (k_spec_run)
+    const bool spec_fused = spec && spec_run_fits(B, N, ve ? kp1 : 2);
+    auto spec_run = [&](int phase, int kstart, int kend, bool with_ve, bool all_cadence) -> int {
       StepCtl c = ctl;
       c.phase = phase;
       SpecStepArgs sa;
@@ -1681,10 +1679,11 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       sa.st = st; sa.ctl = c; sa.tr = tr; sa.S = S;
       sa.partials = p->sp_part.as<double>(); sa.counters = p->sp_cnt.as<unsigned>();
       int rc = 0;
-      RUN(ctx, "spec_steps", rc = launch_spec_steps(sa, n, mask, track ? 1 : 0,
-                                                    p->best.as<double>(), s));
-      if (rc) return fail(ctx, REDVE_E_CUDA, "spec_steps: %s", cudaGetErrorString((cudaError_t)rc));
-      kk += n;
+      RUN(ctx, "spec_run", rc = launch_spec_run(sa, va, kstart, kend, clen, with_ve ? 1 : 0,
+                                                all_cadence ? 1 : 0, track ? 1 : 0,
+                                                p->best.as<double>(), s));
+      if (rc) return fail(ctx, REDVE_E_CUDA, "spec_run: %s", cudaGetErrorString((cudaError_t)rc));
+      kk += kend - kstart;
       return REDVE_OK;
     };
 
@@ -1699,13 +1698,10 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
     const int check_every = (cfg->tol > 0 || !p->fourier) ? 1 : 8;  // CG steps stop exactly
 
     int k = 0;
-    if (!ve && spec_fused) {
-      while (k < budget) {
-        const int n = budget - k < 32 ? budget - k : 32;
-        int r = spec_steps(PH_MAIN, n, k, false);
-        if (r) return r;
-        k += n;
-      }
+    if (spec_fused) {
+      int r = spec_run(PH_MAIN, 0, budget, ve, false);
+      if (r) return r;
+      k = budget;
     } else if (!ve) {
       while (k < budget) {
         int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
@@ -1721,19 +1717,12 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       int cycles = 0;
       while (true) {
         int n = 0;
-        if (spec_fused) {
-          n = budget - k < clen ? budget - k : clen;
-          int r = spec_steps(PH_MAIN, n, k, false);
+        for (int i = 0; i < clen; ++i) {
+          int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
           if (r) return r;
-          k += n;
-        } else {
-          for (int i = 0; i < clen; ++i) {
-            int r = step(PH_MAIN, ((k + 1) % log_every) == 0);
-            if (r) return r;
-            ++k;
-            ++n;
-            if (k >= budget) break;
-          }
+          ++k;
+          ++n;
+          if (k >= budget) break;
         }
         if (n == clen) {
           RUN(ctx, "gram", launch_gram(va, s));
@@ -1755,8 +1744,8 @@ int redve_solve(redve_problem* p, const redve_solve_config* cfg, const double* x
       }
     }
     if (spec_fused) {
-      for (int i = 0; i < stab; i += 32) {
-        int r = spec_steps(PH_STAB, stab - i < 32 ? stab - i : 32, 0, true);
+      if (stab > 0) {
+        int r = spec_run(PH_STAB, 0, stab, false, true);
         if (r) return r;
       }
     } else {

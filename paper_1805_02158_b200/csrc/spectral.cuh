@@ -59,12 +59,14 @@ struct SpecCostArgs {
 int spec_chunks(int B, long long N);
 void launch_spec_step(const SpecStepArgs& a, cudaStream_t s);
 void launch_spec_cost(const SpecCostArgs& a, cudaStream_t s);
-// nsteps spectral steps in one cluster launch per image (bit i of cadence_mask:
-// step i records the cost; copy_best: cadence steps copy an improved iterate to
-// best); spec_steps_fits says whether the batch / size qualifies
-bool spec_steps_fits(int B, long long N);
-int launch_spec_steps(const SpecStepArgs& a, int nsteps, unsigned cadence_mask, int copy_best,
-                      double* best, cudaStream_t s);
+// The spectral schedule on chip, one cluster launch per image: steps k in
+// [kstart, budget) (cadence by ctl.log_every, or every step with all_cadence),
+// with the VE step (va) after each full cycle of clen steps when ve != 0;
+// copy_best: cadence steps copy an improved iterate to best.  spec_run_fits
+// says whether the batch / size / kappa qualify.
+bool spec_run_fits(int B, long long N, int kp1);
+int launch_spec_run(const SpecStepArgs& a, const VeArgs& va, int kstart, int budget, int clen,
+                    int ve, int all_cadence, int copy_best, double* best, cudaStream_t s);
 // real [B][N] (plain stride N) -> complex [B] at out + b*odist (imag 0), non-finite flag
 void launch_spec_pack(const double* x, int B, long long N, cd* out, long long odist, int* bad,
                       cudaStream_t s);

@@ -113,11 +113,12 @@ def test_spectral_graph_reuse_and_nonfinite(rv):
 
 @pytest.mark.parametrize("B,n", [(1, 256), (3, 64), (2, 128)])
 @pytest.mark.parametrize("method,stab", [("fp", 0), ("fp-ve", 0), ("fp-ve", 3)])
-def test_fused_cluster_steps_equal_per_step_kernels(rv, monkeypatch, B, n, method, stab):
-    """Small batches run the spectral steps of a cycle in one cluster launch
-    (k_spec_steps); REDVE_SPEC_FUSED=0 launches k_spec_step per step.  The
-    step arithmetic is the same, so the iterates agree bit for bit; the
-    recorded sums are reduced over DSMEM in another fixed order (1e-13)."""
+def test_fused_cluster_run_equals_launch_schedule(rv, monkeypatch, B, n, method, stab):
+    """Small batches run the whole spectral schedule in one cluster launch per
+    image (k_spec_run); REDVE_SPEC_FUSED=0 issues it as per-step / per-VE
+    launches.  The steps are the same arithmetic; sums (step norms, costs,
+    the VE Gram) are reduced in another fixed order, so the iterates agree to
+    rounding and every decision (records, accepted cycles) is identical."""
     from paper_1805_02158_b200.synth import voronoi_scene
 
     op = rv.Blur(rv.make_psf("uniform", 9), (n, n))
@@ -129,12 +130,13 @@ def test_fused_cluster_steps_equal_per_step_kernels(rv, monkeypatch, B, n, metho
     for flag in ("1", "0"):
         monkeypatch.setenv("REDVE_SPEC_FUSED", flag)
         batch = rv.RedBatch(op, ys, SQRT2, 0.02, rv.GaussianFilter(), truths)
-        res = batch.solve(ys, cfg)
-        out[flag] = res
+        out[flag] = batch.solve(ys, cfg)
     a, b = out["1"], out["0"]
-    np.testing.assert_array_equal(a.x.cpu().numpy(), b.x.cpu().numpy())
+    xa, xb = a.x.cpu().numpy(), b.x.cpu().numpy()
+    assert np.linalg.norm(xa - xb) <= 1e-12 * np.linalg.norm(xb)
     np.testing.assert_array_equal(a.n_records, b.n_records)
-    np.testing.assert_allclose(a.step_norm, b.step_norm, rtol=1e-12, equal_nan=True)
+    np.testing.assert_array_equal(a.n_cycles, b.n_cycles)
+    np.testing.assert_array_equal(np.isnan(a.gamma_abs_sum), np.isnan(b.gamma_abs_sum))
+    np.testing.assert_allclose(a.step_norm, b.step_norm, rtol=1e-9, atol=1e-14, equal_nan=True)
     np.testing.assert_allclose(a.cost, b.cost, rtol=1e-12, equal_nan=True)
     np.testing.assert_allclose(a.psnr, b.psnr, rtol=1e-12, equal_nan=True)
-    np.testing.assert_array_equal(a.n_cycles, b.n_cycles)
