@@ -522,6 +522,10 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20, ws=8):
         # implementation streams 24 stored weight planes per sweep on top
         # (pw_implementation_bytes), which this does not credit
         "patch_weighted": B * N * s * (2 + 2 * iters),
+        # spectral route on chip (k_spec_run, one launch per solve): per step the
+        # spectrum in / out and the constants m, Xb (complex, 16 B), per cycle
+        # the VE window twice (Gram, recombination)
+        "spec_run": B * N * 16 * (4 * BUDGET + 2 * (kp1 + 1) * (BUDGET // kp1)),
         # slab primitives of the spatial solve (configs[4])
         "normal_matvec": 2 * B * N * s,      # read w, write out
         "vec_reduce": 2 * B * N * s,         # read x, y
