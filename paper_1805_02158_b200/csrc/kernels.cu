@@ -28,6 +28,15 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // --------------------------------------------------------------- setup
+// Kernels that need more than 48 KB of dynamic shared memory raise their limit
+// at first launch (next to the launch), so context creation only clears any
+// stale error state.
+int configure_kernels() {
+  cudaGetLastError();
+  return (int)cudaSuccess;
+}
+
+// raise a kernel's dynamic shared-memory limit to what the device allows
 template <class K>
 static cudaError_t allow_big_smem(K kernel, int optin) {
   if (optin < 0) {
@@ -40,14 +49,6 @@ static cudaError_t allow_big_smem(K kernel, int optin) {
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               optin - (int)fa.sharedSizeBytes);
-}
-int configure_kernels() {
-  int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaError_t e = cudaSuccess, r;
-  cudaGetLastError();
-  return (int)e;
 }
 
 __global__ void k_twiddles(cd* tw, int L) {
@@ -518,12 +519,10 @@ __device__ __noinline__ void mgs_block(const VeArgs& a, int b) {
   ImgState& s = a.st[b];
   __shared__ double s_red[32];
   __shared__ double R[MAXKP1][MAXKP1];
-  __shared__ int s_stop;
   const int n = a.kp1;
   const long long N = a.N;
   double* Q = a.qscratch + (long long)b * n * N;
   if (threadIdx.x < MAXKP1 * MAXKP1) (&R[0][0])[threadIdx.x] = 0.0;
-  if (threadIdx.x == 0) s_stop = 0;
   __syncthreads();
   const int s0 = s.start + a.m;
   int rank = n;
