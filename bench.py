@@ -533,6 +533,7 @@ def algorithmic_bytes(kind, B, N, s=8, kp1=KAPPA + 1, npos=24, iters=20, ws=8):
         "fidelity": B * N * s + B * N * s // 9,
         "window_gram": (kp1 + 1) * B * N * s,
         "window_combine": (kp1 + 1) * B * N * s,
+        "halo_push": 2 * B * N * s,          # read the slab, write it (+ 2 halo strips)
     }
     return table.get(kind)
 
@@ -864,7 +865,7 @@ def run_spatial(a):
 
     import paper_1805_02158_b200 as rv
     from paper_1805_02158_b200 import _native as nat
-    from paper_1805_02158_b200.spatial import SpatialProblem, TorchComm, solve_spatial
+    from paper_1805_02158_b200.spatial import PeerComm, SpatialProblem, solve_spatial
     from paper_1805_02158_b200.synth import voronoi_scene
 
     c = CONFIGS[4]
@@ -881,7 +882,9 @@ def run_spatial(a):
     x0 = np.asarray(op.adjoint(y))            # zero-filled adjoint initialisation
     del clean
     den = product_denoiser(c)
-    comm = TorchComm(device="cpu" if shared else "cuda")  # gloo carries host tensors
+    # halos by peer-memory stores; allreduces on gloo (host tensors) when the
+    # ranks share one GPU, NCCL otherwise
+    comm = PeerComm(device="cpu" if shared else "cuda")
     prob = SpatialProblem(op, y, c["sigma"], ALPHA, den, comm=comm, reference=truth)
     cfg = rv.SolveConfig(method="fp-ve", ve_method="rre", m=0, kappa=KAPPA,
                          max_inner_steps=SPATIAL_BUDGET)
@@ -992,6 +995,14 @@ def run_spatial(a):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        # drop the peer mappings of the neighbours' buffers on every rank before
+        # any rank exits (a producer must outlive its IPC consumers)
+        del prob2
+        gc.collect()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.ipc_collect()  # release what the neighbours have let go of
+        barrier()
         dist.destroy_process_group()
 
 

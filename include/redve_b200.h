@@ -225,6 +225,20 @@ int redve_sr_normal_matvec(redve_ctx* ctx, const redve_operator_desc* op, double
 int redve_vec_dot(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
 int redve_vec_dist2(redve_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
 int redve_vec_axpby(redve_ctx* ctx, int64_t n, double a, const double* x, double b, double* y);
+/* halo exchange over peer memory (replaces the neighbour send/recv of the
+ * slab ring; reference: none, the reference solves one image on one CPU).
+ * x: DEVICE [rows][W] slab; ext: this rank's DEVICE [rows + 2 halo][W] buffer,
+ * interior rows [halo, halo + rows) <- x; prev_bot: the previous rank's bottom
+ * halo (its ext + (halo + rows_prev) W) <- x's first halo rows; next_top: the
+ * next rank's top halo (its ext) <- x's last halo rows.  Peer pointers are
+ * CUDA-IPC mappings of the neighbours' buffers; for one rank pass this rank's
+ * own ext halos (periodic wrap).  Ordering against the neighbours' readers is
+ * the caller's (stream sync + barrier on both sides). */
+/* let the context's device load/store the memory of device `peer` (NVLink P2P);
+ * idempotent, REDVE_E_UNSUPPORTED when the pair has no peer access */
+int redve_enable_peer_access(redve_ctx* ctx, int peer);
+int redve_halo_push(redve_ctx* ctx, int rows, int W, int halo, const double* x, double* ext,
+                    double* prev_bot, double* next_top);
 /* sum over interior rows [halo, halo + rows) of ((H x) - y_up)^2 at lattice points */
 int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, int W, int row0,
                       int Hg, int halo, int rows, const double* x_ext, const double* yup_ext,

@@ -109,6 +109,9 @@ SYMBOLS = {
     "redve_vec_dist2": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, _dp]),
     "redve_vec_axpby": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_double,
                                   C.c_void_p]),
+    "redve_enable_peer_access": (C.c_int, [C.c_void_p, C.c_int]),
+    "redve_halo_push": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]),
     "redve_sr_fidelity": (C.c_int, [C.c_void_p, C.POINTER(OperatorDesc), C.c_int, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, _dp]),
     "redve_window_gram": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p, _dp]),

@@ -2022,6 +2022,33 @@ int redve_vec_axpby(redve_ctx* ctx, int64_t n, double a, const double* x, double
   return REDVE_OK;
 }
 
+int redve_enable_peer_access(redve_ctx* ctx, int peer) {
+  if (!ctx) return REDVE_E_VALUE;
+  if (peer == ctx->device) return REDVE_OK;
+  int can = 0;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceCanAccessPeer(&can, ctx->device, peer));
+  if (!can) return fail(ctx, REDVE_E_UNSUPPORTED, "no peer access %d -> %d", ctx->device, peer);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return REDVE_OK;
+  }
+  CK(e);
+  return REDVE_OK;
+}
+
+int redve_halo_push(redve_ctx* ctx, int rows, int W, int halo, const double* x, double* ext,
+                    double* prev_bot, double* next_top) {
+  if (rows <= 0 || W <= 0 || halo < 0 || halo > rows)
+    return fail(ctx, REDVE_E_SHAPE, "halo_push: rows=%d W=%d halo=%d", rows, W, halo);
+  if (!x || !ext || (halo > 0 && (!prev_bot || !next_top)))
+    return fail(ctx, REDVE_E_VALUE, "halo_push: null buffer");
+  RUN(ctx, "halo_push", launch_halo_push(rows, W, halo, x, ext, prev_bot, next_top, ctx->stream));
+  CKL();
+  return REDVE_OK;
+}
+
 int redve_sr_fidelity(redve_ctx* ctx, const redve_operator_desc* op, int Hext, int W, int row0,
                       int Hg, int halo, int rows, const double* x_ext, const double* yup_ext,
                       double* out) {

@@ -59,6 +59,41 @@ void launch_vec_axpby(long long n, double a, const double* x, double b, double* 
   k_vec_axpby<<<nblocks(n), 256, 0, s>>>(n, a, x, b, y);
 }
 
+// Halo push over peer memory: the slab x [rows][W] goes into the interior of
+// this rank's extended buffer, and in the same pass its first `halo` rows are
+// stored into the previous rank's bottom halo and its last `halo` rows into
+// the next rank's top halo (pointers opened over CUDA IPC, or into this
+// rank's own buffer for a single-rank periodic wrap).  16-byte accesses when
+// every row start is 16-byte aligned.
+template <typename V>
+__global__ void k_halo_push(long long rows, long long Wv, long long halo, const V* x, V* ext,
+                            V* prev_bot, V* next_top) {
+  const long long n = rows * Wv;
+  const long long lo = halo * Wv, hi = (rows - halo) * Wv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const V v = x[i];
+    ext[lo + i] = v;
+    if (i < lo) prev_bot[i] = v;
+    if (i >= hi) next_top[i - hi] = v;
+  }
+}
+void launch_halo_push(int rows, int W, int halo, const double* x, double* ext, double* prev_bot,
+                      double* next_top, cudaStream_t s) {
+  const bool v2 = (W % 2 == 0) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(ext) |
+                                    reinterpret_cast<uintptr_t>(prev_bot) |
+                                    reinterpret_cast<uintptr_t>(next_top)) % 16 == 0);
+  if (v2) {
+    const long long Wv = W / 2;
+    k_halo_push<double2><<<nblocks((long long)rows * Wv), 256, 0, s>>>(
+        rows, Wv, halo, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(ext),
+        reinterpret_cast<double2*>(prev_bot), reinterpret_cast<double2*>(next_top));
+  } else {
+    k_halo_push<double><<<nblocks((long long)rows * W), 256, 0, s>>>(rows, W, halo, x, ext,
+                                                                    prev_bot, next_top);
+  }
+}
+
 // sum over the interior rows [h, h + rows) of ((H x)(u,v) - y_up(u,v))^2 at the
 // GLOBAL measurement lattice ((row0 + u) mod Hg == 0 mod f, v == 0 mod f).
 __global__ void k_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, int f,

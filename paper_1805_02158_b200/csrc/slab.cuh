@@ -12,6 +12,8 @@ void launch_vec_reduce(int op, long long n, const double* x, const double* y, do
                        double* out, cudaStream_t s);  // op 0: dot, 1: squared distance
 void launch_vec_axpby(long long n, double a, const double* x, double b, double* y,
                       cudaStream_t s);
+void launch_halo_push(int rows, int W, int halo, const double* x, double* ext, double* prev_bot,
+                      double* next_top, cudaStream_t s);
 void launch_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, int f,
                      const double* taps, int k, const double* x, const double* yup, double* part,
                      double* out, cudaStream_t s);

@@ -89,7 +89,10 @@ def test_window_gram_decide_combine(pair, method):
 def _native_spatial(H, W, method, budget, ve_method, den_name="median", comm=None):
     from paper_1805_02158_b200 import Median3, PatchWeighted
     from paper_1805_02158_b200.solvers import SolveConfig
-    from paper_1805_02158_b200.spatial import SpatialProblem, TorchComm, solve_spatial
+    from paper_1805_02158_b200.spatial import PeerComm, SpatialProblem, TorchComm, solve_spatial
+
+    if comm == "peer":                     # built inside the rank process
+        comm = PeerComm(device="cpu")
 
     taps, op, truth, y, _, _, x0 = _setup(H, W, "median")
     den = Median3() if den_name == "median" else PatchWeighted(1, 1, 110.0, 3)
@@ -155,6 +158,92 @@ def test_two_ranks_native_solve():
     q = ctx.Queue()
     port = _free_port()
     args = (H, W, "fp-ve", budget, "rre")
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, args)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert not isinstance(out[r], str), out[r]
+    for k in range(4):
+        np.testing.assert_array_equal(out[0][k], out[1][k])
+    _check(out[0], H, W, "fp-ve", budget, "rre")
+
+
+# ---- peer-memory halo exchange (PeerComm / redve_halo_push) ----------------
+def test_single_rank_peer_push_solve():
+    from paper_1805_02158_b200.spatial import PeerComm
+
+    got = _native_spatial(96, 90, "fp-ve", 14, "rre", comm=PeerComm())
+    ref = _native_spatial(96, 90, "fp-ve", 14, "rre")
+    for k in range(4):
+        np.testing.assert_array_equal(got[k], ref[k])  # same halos -> same bits
+
+
+def _push_worker(rank, world, port, q, args):
+    """Every rank pushes a slab whose values encode (global row, column); the
+    extended buffers must then hold the ring's rows exactly."""
+    import torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1805_02158_b200.spatial import PeerComm, SlabLayout
+
+        H, W, factor, halo = args
+        comm = PeerComm(device="cpu")
+        lay = SlabLayout(H, W, factor, world, rank, halo)
+        g = torch.arange(H, dtype=torch.float64, device="cuda")[:, None] * 1000 + \
+            torch.arange(W, dtype=torch.float64, device="cuda")[None, :]
+        ext = torch.full((lay.Hext, W), -1.0, dtype=torch.float64, device="cuda")
+        bad = 0
+        for rnd in range(3):                       # repeated pushes reuse the mappings
+            x = g[lay.start: lay.stop] + rnd
+            comm.push(ext, x, halo, lay.rows)
+            want = g[torch.tensor(lay.ext_rows(), device="cuda")] + rnd
+            bad += int((ext != want).sum().item())
+        q.put((rank, (bad, lay.rows, hasattr(ext, "_redve_peer"))))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,H,W,halo", [(2, 99, 47, 4), (3, 99, 64, 3), (2, 60, 10, 30)])
+def test_peer_push_ring(world, H, W, halo):
+    """Ragged slabs (99 rows / factor 3 does not split evenly), odd and even
+    widths (scalar and 16-byte paths), and a halo as thick as the slab."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_push_worker, args=(r, world, port, q, (H, W, 3, halo)))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(out[r], str), out[r]
+        assert out[r][0] == 0 and out[r][2]
+    if (world, H) == (2, 99):
+        assert len({out[r][1] for r in range(world)}) > 1  # really ragged (51 / 48)
+
+
+def test_two_ranks_peer_push_solve():
+    """The distributed solve with peer-memory halos equals the send/recv one."""
+    import torch.multiprocessing as mp
+
+    H, W, budget = 96, 90, 14
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = (H, W, "fp-ve", budget, "rre", "median", "peer")
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q, args)) for r in range(2)]
     for p in procs:
         p.start()
