@@ -488,6 +488,32 @@ void launch_col(const ColArgs& a, int npairs, cudaStream_t s) {
 }
 
 // --------------------------------------------------------------- row inverse
+// Epilogue of one image of the pair: x+ = IDFT part + x_b, and the step-norm
+// partials against x_prev (acc[0..2]); all loads issue before the first use.
+template <class F>
+__device__ __forceinline__ void row_inv_image(double* __restrict__ o, const double* __restrict__ bs,
+                                              const double* __restrict__ pv, int t, int T,
+                                              double* acc, F val_of) {
+  double lb[16], lp[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) lb[m] = bs ? __ldg(bs + t + T * m) : 0.0;
+  if (pv) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) lp[m] = __ldg(pv + t + T * m);
+  }
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const double val = val_of(m) + lb[m];
+    o[t + T * m] = val;
+    if (pv) {
+      const double d = val - lp[m];
+      acc[0] = fma(d, d, acc[0]);
+      acc[1] = fma(lp[m], lp[m], acc[1]);
+      acc[2] += isfinite(val) ? 0.0 : 1.0;
+    }
+  }
+}
+
 template <int LW>
 __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
@@ -527,6 +553,21 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
     const double* p1 = (a1 && a.epilogue) ? a.xprev.at(b1, a.st) + (long long)row * W : nullptr;
     const double* bs0 = (a0 && a.base) ? a.base + (long long)b0 * N + (long long)row * W : nullptr;
     const double* bs1 = (a1 && a.base) ? a.base + (long long)b1 * N + (long long)row * W : nullptr;
+    if constexpr (LW > 0) {
+      // One image at a time, all 16 columns: 32 loads in flight per thread and
+      // two memory round trips per CTA instead of four (the epilogue's latency
+      // is the kernel's critical path).  The second image's values wait in the
+      // line buffer, which the transform's last barrier left free; each thread
+      // parks and re-reads its own slots (conflict-free, no barrier).
+      double* park = reinterpret_cast<double*>(s_work) + threadIdx.x;
+      const int PS = blockDim.x;
+      if (o1) {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) park[m * PS] = v[m].y;
+      }
+      if (o0) row_inv_image(o0, bs0, p0, t, T, acc, [&](int m) { return v[m].x; });
+      if (o1) row_inv_image(o1, bs1, p1, t, T, acc + 3, [&](int m) { return park[m * PS]; });
+    } else {
     // four batches of 4 columns: all loads of a batch issue before its stores
     // (8-column batches spilled at the 128-register cap)
 #pragma unroll
@@ -567,6 +608,7 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
           }
         }
       }
+    }
     }
   }
   if (!a.epilogue) return;
