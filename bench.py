@@ -616,8 +616,8 @@ def _reduce_max(t, world, shared):
     return float(t.item())
 
 
-def settle_solves(solve, tol=0.03, budget_s=3.0):
-    """Extra untimed solves after the W warm-up ones until two consecutive solves
+def settle_solves(solve, tol=0.01, budget_s=4.0):
+    """Extra untimed solves after the W warm-up ones until three consecutive solves
     take the same device time (within ``tol``), at most ``budget_s`` seconds.
     On a freshly acquired box the first second of GPU work ran up to 2x slow
     (a first bench on a fresh box after pytest measured 45.6 ms per configs[1]
@@ -626,7 +626,7 @@ def settle_solves(solve, tol=0.03, budget_s=3.0):
     import torch
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prev, n, t0 = None, 0, time.time()
+    hist, n, t0 = [], 0, time.time()
     while time.time() - t0 < budget_s:
         e0.record()
         solve()
@@ -634,9 +634,9 @@ def settle_solves(solve, tol=0.03, budget_s=3.0):
         torch.cuda.synchronize()
         n += 1
         ms = e0.elapsed_time(e1)
-        if prev is not None and abs(ms - prev) <= tol * prev:
+        hist.append(ms)
+        if len(hist) >= 3 and max(hist[-3:]) - min(hist[-3:]) <= tol * min(hist[-3:]):
             break
-        prev = ms
     return n
 
 
@@ -690,11 +690,15 @@ def run_native(a):
     l0 = nat.kernel_launches()
     tw0 = time.time()
     e0.record(stream)
+    marks = []  # per-step boundaries (diagnostic: a slow step shows up by itself)
     for _ in range(a.steps):
         res = batch.solve(x0, cfg)
+        marks.append(torch.cuda.Event(enable_timing=True))
+        marks[-1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks.mark(tw0, time.time())
+    step_ms = [round(p.elapsed_time(q), 3) for p, q in zip([e0] + marks[:-1], marks)]
     l1 = nat.kernel_launches()
     barrier()
     clk = clocks.stop()
@@ -846,6 +850,7 @@ def run_native(a):
                                      zip(*phases))}},
             "gpu_launches": int(launches),
             "settle_solves": settle,
+            "step_ms": step_ms,
             "methods": methods,
             "roofline": roof,
             "step_roofline": step_roof,

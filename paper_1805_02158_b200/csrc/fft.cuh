@@ -345,4 +345,28 @@ __device__ __forceinline__ void load_twiddles(cd* dst, const cd* src, int L) {
   for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = ldg_cd(src + i);
 }
 
+// The same in two halves, so a kernel can issue the global loads before a
+// dependent load chain (image state -> ring slot -> tile) and park them in
+// shared memory after it: the first two entries per thread travel in registers.
+struct TwiddleRegs {
+  cd r[2];
+};
+__device__ __forceinline__ TwiddleRegs twiddles_issue(const cd* src, int L) {
+  TwiddleRegs q;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    q.r[j] = i < L ? ldg_cd(src + i) : cd{0.0, 0.0};
+  }
+  return q;
+}
+__device__ __forceinline__ void twiddles_park(cd* dst, const cd* src, int L, const TwiddleRegs& q) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < L) dst[i] = q.r[j];
+  }
+  for (int i = threadIdx.x + 2 * blockDim.x; i < L; i += blockDim.x) dst[i] = ldg_cd(src + i);
+}
+
 }  // namespace redve

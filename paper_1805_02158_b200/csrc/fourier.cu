@@ -90,6 +90,10 @@ constexpr int RF_BATCH = 10;
 template <int LW, int DK>
 __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
+  const int ntw = LW > 0 ? tw_stage_size(LW) : a.W;
+  // twiddle loads first: they do not depend on the image state, so they overlap
+  // the tile's (state -> slot -> address) latency chain; parked after the tile
+  const TwiddleRegs twq = twiddles_issue(LW > 0 ? a.tws : a.tw, ntw);
   const bool a0 = takes_step(a.st[b0], a.phase);
   const bool a1 = b1 < a.B && takes_step(a.st[b1], a.phase);
   if (!a0 && !a1) return;
@@ -98,14 +102,10 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
   const int T = LW > 0 ? LW / 16 : threads_per_line(W);
   const int R = DK == DN_CONV ? a.dn.ksize / 2 : (DK == DN_MEDIAN3 ? 1 : 0);
   const int ks = DK == DN_CONV ? a.dn.ksize : 0;
-  const int ntw = LW > 0 ? tw_stage_size(LW) : W;
   cd* s_tw = reinterpret_cast<cd*>(f_smem);
   double* s_taps = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)));
   cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)) +
                                      al16f((size_t)a.dn.ksize * a.dn.ksize * sizeof(double)));
-  load_twiddles(s_tw, LW > 0 ? a.tws : a.tw, ntw);
-  if (DK == DN_CONV)
-    for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
   const double* x0 = a0 ? a.xin.at(b0, a.st) : nullptr;
   const double* x1 = a1 ? a.xin.at(b1, a.st) : nullptr;
   const int r0 = blockIdx.x * a.lpc;
@@ -144,6 +144,9 @@ __global__ void __launch_bounds__(256) k_row_fwd(RowFwdArgs a) {
       st_cd(s_work + tl.at(i, c), cd{x0 ? __ldg(x0 + o) : 0.0, x1 ? __ldg(x1 + o) : 0.0});
     }
   }
+  twiddles_park(s_tw, LW > 0 ? a.tws : a.tw, ntw, twq);
+  if (DK == DN_CONV)
+    for (int i = threadIdx.x; i < ks * ks; i += blockDim.x) s_taps[i] = a.dn.taps[i];
   __syncthreads();
   const int line = threadIdx.x / T, t = threadIdx.x - line * T;
   const int row = r0 + line;
@@ -517,23 +520,16 @@ __device__ __forceinline__ void row_inv_image(double* __restrict__ o, const doub
 template <int LW>
 __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
   const int p = blockIdx.y, b0 = 2 * p, b1 = 2 * p + 1;
-  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
-  const bool a0 = takes_step(a.st[b0], phase);
-  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
-  if (!a0 && !a1) return;
   const int W = LW > 0 ? LW : a.W;
   const int H = a.H;
   const int T = LW > 0 ? LW / 16 : threads_per_line(W);
   const long long N = (long long)H * W;
-  const int ntw = LW > 0 ? tw_stage_size(LW) : W;
-  cd* s_tw = reinterpret_cast<cd*>(f_smem);
-  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)));
-  double* s_red = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)) +
-                                            (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
-  load_twiddles(s_tw, LW > 0 ? a.tws : a.tw, ntw);
   const int line = threadIdx.x / T, t = threadIdx.x - line * T;
   const int row = blockIdx.x * a.lpc + line;
   const bool valid = row < H;
+  // the spectrum rows first: their address does not depend on the image state,
+  // so the loads are in flight while the state (a dependent L2 round trip) and
+  // the twiddles arrive
   const cd* zr = a.Z + ((long long)p * H + (valid ? row : 0)) * W;
   cd v[16];
 #pragma unroll
@@ -541,6 +537,17 @@ __global__ void __launch_bounds__(128, 4) k_row_inv(RowInvArgs a) {
     const int c = t + T * m;
     v[m] = (valid && c < W) ? ld_cd(zr + c) : cd{0.0, 0.0};
   }
+  const int ntw = LW > 0 ? tw_stage_size(LW) : W;
+  const TwiddleRegs twq = twiddles_issue(LW > 0 ? a.tws : a.tw, ntw);
+  const int phase = a.epilogue ? a.ctl.phase : PH_SETUP;
+  const bool a0 = takes_step(a.st[b0], phase);
+  const bool a1 = b1 < a.B && takes_step(a.st[b1], phase);
+  if (!a0 && !a1) return;
+  cd* s_tw = reinterpret_cast<cd*>(f_smem);
+  cd* s_work = reinterpret_cast<cd*>(f_smem + al16f(ntw * sizeof(cd)));
+  double* s_red = reinterpret_cast<double*>(f_smem + al16f(ntw * sizeof(cd)) +
+                                            (size_t)a.lpc * RowLayout::stride_for(W) * sizeof(cd));
+  twiddles_park(s_tw, LW > 0 ? a.tws : a.tw, ntw, twq);
   __syncthreads();
   RowLayout lay{RowLayout::stride_for(W)};
   fft_dispatch<LW, true>(v, s_work, s_tw, W, t, line, lay);
