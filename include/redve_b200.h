@@ -183,6 +183,13 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
                          double sigma, double alpha, const double* reference,
                          redve_problem** out);
 void redve_problem_destroy(redve_problem* p);
+/* New measurements (and PSNR reference) for an existing problem: the same
+ * operator, denoiser, sigma, alpha and shapes as a fresh RedObjective
+ * (objective.py:61-74 recomputes H^T y / sigma^2 per object), but the device
+ * buffers and the captured solve graph are kept, so a stream of batches pays
+ * neither allocation nor graph capture.  reference must be given iff the
+ * problem was created with one.  y / reference: DEVICE, shapes as in create. */
+int redve_problem_set_measurements(redve_problem* p, const double* y, const double* reference);
 /* Number of times redve_solve captured (and instantiated) its CUDA graph for
  * this problem.  Repeated solves with the same configuration replay one
  * capture whatever x0 / x_out buffers they pass (no reference counterpart:

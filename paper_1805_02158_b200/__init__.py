@@ -20,6 +20,7 @@ from .extrapolation import (METHODS, MPE, RRE, SVDMPE, ExtrapolationResult, Extr
 from .imaging import (Blur, BlurDownsample, Psf, as_image, convolve_circular, degrade, dft2,
                       embed_psf, gaussian_noise, idft2, make_psf, psf_spectrum, psnr,
                       synthetic_image)
+from .pipeline import solve_stream
 from .objective import (RedObjective, as_fixed_point_problem, check_local_homogeneity,
                         check_passivity, default_step_size)
 from .solvers import (FixedPointProblem, IterationTrace, LinearFixedPointProblem, SolveConfig,

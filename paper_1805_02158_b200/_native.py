@@ -95,6 +95,7 @@ SYMBOLS = {
                                        C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
                                        C.c_double, C.c_void_p, C.POINTER(C.c_void_p)]),
     "redve_problem_destroy": (None, [C.c_void_p]),
+    "redve_problem_set_measurements": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "redve_problem_graph_captures": (C.c_uint64, [C.c_void_p]),
     "redve_fp_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "redve_fp_step_denoised": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -166,17 +167,24 @@ def _torch():
 
 
 def context(device: int | None = None):
-    """Per-device native context, bound to torch's current stream."""
+    """Native context of (device, calling thread), bound to torch's current stream.
+
+    A context is not thread-safe but distinct contexts run concurrently
+    (include/redve_b200.h), so every host thread gets its own: that is what lets
+    ``pipeline.solve_stream`` keep several batches in flight."""
+    import threading
+
     torch = _torch()
     dev = torch.cuda.current_device() if device is None else int(device)
     lib = library()
-    if dev not in _ctx:
+    key = (dev, threading.get_ident())
+    if key not in _ctx:
         h = C.c_void_p()
         rc = lib.redve_create(C.byref(h), dev)
         if rc != REDVE_OK:
             raise NativeError(rc, lib.redve_last_error(h).decode())
-        _ctx[dev] = h
-    h = _ctx[dev]
+        _ctx[key] = h
+    h = _ctx[key]
     lib.redve_set_stream(h, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     return h
 

@@ -79,6 +79,31 @@ class RedBatch:
         self._h = h
         self._ctx = ctx
 
+    def set_measurements(self, ys, references=None):
+        """New measurements (and PSNR references) for the same operator, denoiser,
+        sigma and alpha: what a fresh ``RedBatch`` would compute (objective.py:61-74),
+        in this one's device buffers and with its captured solve schedule."""
+        yt, _ = _io.to_device(ys)
+        if yt.dim() == 2:
+            yt = yt.unsqueeze(0)
+        if tuple(yt.shape) != tuple(self.y.shape):
+            raise ShapeMismatch(f"expected measurements of shape {tuple(self.y.shape)}")
+        rt = None
+        if references is not None:
+            rt, _ = _io.to_device(references)
+            if rt.dim() == 2:
+                rt = rt.unsqueeze(0)
+            rt = rt.contiguous()
+        if (rt is None) != (self.ref is None):
+            raise ValueError("a RedBatch keeps its PSNR-reference mode (created "
+                             f"{'without' if self.ref is None else 'with'} references)")
+        yt = yt.contiguous()
+        nat.context()  # bind the context to the caller's current stream
+        nat.check(nat.library().redve_problem_set_measurements(self._h, nat.dptr(yt), nat.dptr(rt)),
+                  self._ctx)
+        self.y, self.ref, self._y_src = yt, rt, ys
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:

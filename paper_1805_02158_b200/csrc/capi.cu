@@ -823,6 +823,51 @@ int redve_operator_adjoint(redve_ctx* ctx, const redve_operator_desc* op, int B,
 }
 
 // ------------------------------------------------------------------ problem
+// Everything of a problem that depends on the measurements (and the PSNR
+// reference): y, H^T y / sigma^2 (objective.py:70), x_b, ||y||^2, fresh image
+// state.  Buffers, operator constants and the captured solve graph do not.
+static int problem_measurements(redve_problem* p, const double* y, const double* reference) {
+  redve_ctx* ctx = p->ctx;
+  const cudaStream_t s = ctx->stream;
+  const int B = p->B, H = p->H, W = p->W;
+  const long long Ny = (long long)p->Hy * p->Wy;
+  CK(cudaMemcpyAsync(p->y.p, y, sizeof(double) * Ny * B, cudaMemcpyDeviceToDevice, s));
+  if (reference)
+    CK(cudaMemcpyAsync(p->ref.p, reference, sizeof(double) * p->N * B, cudaMemcpyDeviceToDevice,
+                       s));
+  RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), B, s));
+  const double is2 = 1.0 / (p->sigma * p->sigma);
+  if (!p->fourier) {
+    RUN(ctx, "upsample_corr", launch_upsample_corr(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                                   p->op.factor, p->htaps.as<double>(),
+                                                   p->op.ksize, is2, s));
+  } else {  // rank-one PSFs as two 1-D passes
+    bool done = false;
+    if (p->separable)
+      RUN(ctx, "conv", done = launch_conv_rank1(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                                p->hsep.as<double>(), p->op.ksize, 1, is2, s));
+    if (!done)
+      RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W,
+                                   p->htaps.as<double>(), p->op.ksize, 1, is2, s));
+  }
+  CKL();
+  if (p->fourier) {
+    // x_b = IDFT(DFT(H^T y / sigma^2) / d)
+    DenoiseArgs ident{DN_IDENTITY, 0, 0, nullptr};
+    StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
+    TraceBufs tr;
+    memset(&tr, 0, sizeof(tr));
+    int r = fourier_pipeline(p, plain(p->hty.as<double>(), p->N), ident, 1.0,
+                             plain(p->xb.as<double>(), p->N), nullptr, 0, plain(nullptr, p->N),
+                             ctl, tr, 1, PH_SETUP);
+    if (r) return r;
+    RUN(ctx, "sumsq", launch_sumsq(p->y.as<double>(), Ny, B, p->yy.as<double>(), s));
+    CKL();
+  }
+  p->sp_ready = false;  // spectral constants hold DFT(x_b), DFT(y), DFT(ref)
+  return REDVE_OK;
+}
+
 int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
                          const redve_denoiser_desc* dn, int B, int H, int W, const double* y,
                          double sigma, double alpha, const double* reference,
@@ -958,15 +1003,11 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     PK(cudaMemcpyAsync(p->dntaps.p, dn->taps, db, cudaMemcpyHostToDevice, s));
   const long long Ny = (long long)p->Hy * p->Wy;
   PK(p->y.ensure(sizeof(double) * Ny * B));
-  PK(cudaMemcpyAsync(p->y.p, y, sizeof(double) * Ny * B, cudaMemcpyDeviceToDevice, s));
   if (reference) {
     p->has_ref = true;
     PK(p->ref.ensure(sizeof(double) * p->N * B));
-    PK(cudaMemcpyAsync(p->ref.p, reference, sizeof(double) * p->N * B, cudaMemcpyDeviceToDevice,
-                       s));
   }
   PK(p->state.ensure(sizeof(ImgState) * B));
-  RUN(ctx, "init_state", launch_init_state(p->state.as<ImgState>(), B, s));
   int nblk_row = (H + p->lpc_row - 1) / p->lpc_row;
   int nblk_cost = (H + cost_rows(H) - 1) / cost_rows(H);
   int nblk_fp = (H + cost_fp_rows(W) - 1) / cost_fp_rows(W);
@@ -1015,23 +1056,7 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
   }
   PK(p->cnt_rec.ensure(sizeof(unsigned) * (B + 1)));
   PK(cudaMemsetAsync(p->cnt_rec.p, 0, sizeof(unsigned) * (B + 1), s));
-  // H^T y / sigma^2 (objective.py:70)
   PK(p->hty.ensure(sizeof(double) * p->N * B));
-  if (!p->fourier) {
-    RUN(ctx, "upsample_corr", launch_upsample_corr(p->y.as<double>(), p->hty.as<double>(), B, H, W,
-                                                   op->factor, p->htaps.as<double>(), op->ksize,
-                                                   1.0 / (sigma * sigma), s));
-  } else {  // rank-one PSFs as two 1-D passes
-    bool done = false;
-    if (p->separable)
-      RUN(ctx, "conv", done = launch_conv_rank1(p->y.as<double>(), p->hty.as<double>(), B, H, W,
-                                                p->hsep.as<double>(), op->ksize, 1,
-                                                1.0 / (sigma * sigma), s));
-    if (!done)
-      RUN(ctx, "conv", launch_conv(p->y.as<double>(), p->hty.as<double>(), B, H, W,
-                                   p->htaps.as<double>(), op->ksize, 1, 1.0 / (sigma * sigma), s));
-  }
-  PK(cudaGetLastError());
   if (p->fourier) {
     p->twH = ctx->tw(H);
     p->twW = ctx->tw(W);
@@ -1046,22 +1071,15 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
     PK(cudaGetLastError());
     PK(p->Z.ensure(sizeof(cd) * p->N * p->npairs));
     PK(p->xb.ensure(sizeof(double) * p->N * B));
-    // x_b = IDFT(DFT(H^T y / sigma^2) / d)
-    DenoiseArgs ident{DN_IDENTITY, 0, 0, nullptr};
-    StepCtl ctl{PH_SETUP, 0, 0.0, 1, 0, 0};
-    TraceBufs tr;
-    memset(&tr, 0, sizeof(tr));
-    int r = fourier_pipeline(p, plain(p->hty.as<double>(), p->N), ident, 1.0,
-                             plain(p->xb.as<double>(), p->N), nullptr, 0, plain(nullptr, p->N),
-                             ctl, tr, 1, PH_SETUP);
-    if (r) return bail(r);
     // cost identity on the Fourier route (cost.cu k_cost_fp)
     PK(p->fprev.ensure(sizeof(double) * p->N * B));
     PK(p->yy.ensure(sizeof(double) * B));
-    RUN(ctx, "sumsq", launch_sumsq(p->y.as<double>(), Ny, B, p->yy.as<double>(), s));
-    PK(cudaGetLastError());
     if (dn->kind == REDVE_DN_PATCH || dn->kind == REDVE_DN_FILTERBANK)
       PK(p->fcur.ensure(sizeof(double) * p->N * B));
+  }
+  {
+    const int r = problem_measurements(p, y, reference);
+    if (r) return bail(r);
   }
 #undef PK
   *out = p;
@@ -1069,6 +1087,17 @@ int redve_problem_create(redve_ctx* ctx, const redve_operator_desc* op,
 }
 
 void redve_problem_destroy(redve_problem* p) { delete p; }
+
+int redve_problem_set_measurements(redve_problem* p, const double* y, const double* reference) {
+  if (!p) return REDVE_E_VALUE;
+  redve_ctx* ctx = p->ctx;
+  if (!y) return fail(ctx, REDVE_E_VALUE, "y is null");
+  if ((reference != nullptr) != p->has_ref)
+    return fail(ctx, REDVE_E_VALUE,
+                "a problem keeps its PSNR-reference mode: created %s a reference",
+                p->has_ref ? "with" : "without");
+  return problem_measurements(p, y, reference);
+}
 
 uint64_t redve_problem_graph_captures(const redve_problem* p) { return p ? p->captures : 0; }
 

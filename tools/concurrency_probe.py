@@ -44,14 +44,15 @@ for k in range(2):
     assert lib.redve_create(C.byref(h), 0) == 0
     st = torch.cuda.Stream()
     lib.redve_set_stream(h, C.c_void_p(st.cuda_stream))
-    saved = nat._ctx.get(0)
-    nat._ctx[0] = h
+    key = (0, threading.get_ident())
+    saved = nat._ctx.get(key)
+    nat._ctx[key] = h
     with torch.cuda.stream(st):
         yb = yd[k * B // 2:(k + 1) * B // 2].clone()
         bt = rv.RedBatch(op, yb, float(np.sqrt(2)), 0.02, rv.Median3())
         for _ in range(2):
             bt.solve(yb, cfg)
-    nat._ctx[0] = saved
+    nat._ctx[key] = saved
     st.synchronize()
     halves.append((h, st, yb, bt))
 
