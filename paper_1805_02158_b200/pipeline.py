@@ -71,20 +71,38 @@ def solve_stream(forward, batches, sigma, alpha, denoiser, config, references=No
             ev.record(copy)
         return out[0], out[1], ev
 
+    class _Now:  # an upload issued inline (future-like)
+        def __init__(self, value):
+            self.value = value
+
+        def result(self):
+            return self.value
+
+    def staged(item):
+        """Needs a host-side staging copy (unpinned input): worth a helper thread."""
+        parts = item if isinstance(item, tuple) else (item,)
+        return any(a is not None and not (isinstance(a, torch.Tensor) and (a.is_cuda or a.is_pinned()))
+                   for a in parts)
+
     slots = [None, None]
     batch = None
     done = None  # (slot tensor, traces, event) of the previous batch
     it = iter(batches)
     with ThreadPoolExecutor(max_workers=1, thread_name_prefix="redve-upload") as pool:
+        def start(item, parity):
+            # pinned / device inputs: the upload is one asynchronous copy, issued
+            # inline; unpinned ones are staged on the helper thread meanwhile
+            return pool.submit(upload, item, parity) if staged(item) else _Now(upload(item, parity))
+
         try:
-            nxt = pool.submit(upload, next(it), 0)
+            nxt = start(next(it), 0)
         except StopIteration:
             return
         i = 0
         while nxt is not None:
             y_dev, x0_dev, ev = nxt.result()
             try:
-                nxt = pool.submit(upload, next(it), (i + 1) & 1)
+                nxt = start(next(it), (i + 1) & 1)
             except StopIteration:
                 nxt = None
             main.wait_event(ev)

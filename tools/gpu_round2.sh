@@ -1,7 +1,7 @@
 # round 2 measurement pass on one box: bench FIRST (fresh-box behaviour), then
 # tests, smoke, reference arm, every config, launch list, ncu captures
-mkdir -p gpurun_out/r02c
-O=gpurun_out/r02c
+O=${O:-gpurun_out/r02f}; mkdir -p $O
+
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,clocks.max.mem --format=csv > $O/smi.txt 2>&1
 timeout 600 python bench.py > $O/bench_first.log 2>&1; echo "rc=$?" >> $O/bench_first.log
 timeout 900 python -m pytest tests -m gpu -q --tb=short -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
