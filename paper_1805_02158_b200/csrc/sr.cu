@@ -349,7 +349,8 @@ union WVec {
 };
 
 template <int SR, typename WT>
-__global__ void __launch_bounds__(256) k_pw_sweep_v(PwArgs a, const double* Din, double* Dout,
+__global__ void __launch_bounds__(256, 5)  // 48 registers: 45.8 -> 43.1 ms per 8192^2 call
+    k_pw_sweep_v(PwArgs a, const double* Din, double* Dout,
                                                     int first, int apply) {
   constexpr int VW = 16 / sizeof(WT), TW = 32 * VW, TH = 8;
   constexpr int X = TW + 2 * SR, Y = TH + 2 * SR, NP = HalfPlane<SR>::NPOS;
