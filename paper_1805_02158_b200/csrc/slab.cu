@@ -101,17 +101,26 @@ __global__ void k_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, i
                            double* part) {
   const int r = k / 2;
   double acc[1] = {0.0};
-  const long long n = (long long)rows * W;
+  // work items: (interior row, lattice column); rows off the lattice drop out a
+  // warp at a time (the lattice test is per row, the columns are all on it)
+  const int ncl = (W + f - 1) / f;
+  const long long n = (long long)rows * ncl;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int u = h + (int)(idx / W), v = (int)(idx % W);
+    const int u = h + (int)(idx / ncl), v = f * (int)(idx % ncl);
     const int g = (int)(((long long)row0 + u) % Hg);
-    if ((g % f) || (v % f)) continue;
+    if (g % f) continue;
     double hx = 0.0;
-    for (int a = 0; a < k; ++a)
-      for (int c = 0; c < k; ++c)
-        hx = fma(taps[a * k + c], x[(long long)wrap(u - (a - r), Hext) * W + wrap(v - (c - r), W)],
-                 hx);
+    for (int a = 0; a < k; ++a) {
+      int ua = u - (a - r);  // within one period of [0, Hext)
+      ua = ua < 0 ? ua + Hext : (ua >= Hext ? ua - Hext : ua);
+      const double* xr = x + (long long)ua * W;
+      for (int c = 0; c < k; ++c) {
+        int vc = v - (c - r);
+        vc = vc < 0 ? vc + W : (vc >= W ? vc - W : vc);
+        hx = fma(taps[a * k + c], xr[vc], hx);
+      }
+    }
     const double d = hx - yup[(long long)u * W + v];
     acc[0] = fma(d, d, acc[0]);
   }
@@ -122,7 +131,7 @@ __global__ void k_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, i
 void launch_fidelity(int Hext, int W, int row0, int Hg, int h, int rows, int f,
                      const double* taps, int k, const double* x, const double* yup, double* part,
                      double* out, cudaStream_t s) {
-  const int nb = nblocks((long long)rows * W);
+  const int nb = nblocks((long long)rows * ((W + f - 1) / f));
   k_fidelity<<<nb, 256, 0, s>>>(Hext, W, row0, Hg, h, rows, f, taps, k, x, yup, part);
   k_vec_finish<<<1, 32, 0, s>>>(part, nb, out);
 }
