@@ -1,0 +1,192 @@
+// Probe: the PatchWeighted vector sweep rebuilt feature by feature on top of the bare plane read of
+// pw_stream_probe.cu (interior tiles only, no parity: timing of what each ingredient costs).
+//   F_FMA     fp32 -> fp64 convert + DFMA into 4 accumulators (v = a register constant)
+//   F_SMEM    v from the shared D tile (prologue: tile load + barrier), k-major reads like the product kernel
+//   F_MIRROR  the mirrored weights w0_k(p - o_k) spliced from two aligned 16-byte loads
+//   F_STORE   D_out = d / sqrt(d S)
+//   F_NOPRO   (with F_SMEM) skip the prologue: shared reads of an unfilled tile, no barrier
+//   F_NOLDS   (with F_SMEM) prologue + barrier, but v stays a register constant
+//   F_FASTEPI D_out = d * rsqrt(d S) by MUFU.RSQ64H + two Newton steps
+//   F_ROWMAJOR the search window row by row: VW + 6 values of v per row in registers (16-byte shared loads)
+//   F_ICVT    fp32 -> fp64 by two integer multiply-adds (positive normal weights) instead of F2F on the XU pipe
+//   F_SHFL    the second mirrored vector taken from lane + 1's first one (shuffles; lane 31 loads it)
+//   F_ASYNC   prologue by cp.async (16-byte pieces of the aligned tile interior skipped: 8-byte LDGSTS)
+// nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/pw_sweep_probe tools/pw_sweep_probe.cu && /tmp/pw_sweep_probe
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+constexpr int SR = 3, SIDE = 7, NP = 24, VW = 4, TW = 128, TH = 8, X = TW + 2 * SR, Y = TH + 2 * SR;
+enum { F_FMA = 1, F_SMEM = 2, F_MIRROR = 4, F_STORE = 8, F_NOPRO = 16, F_NOLDS = 32, F_FASTEPI = 64, F_ROWMAJOR = 128, F_ASYNC = 256, F_ICVT = 512, F_SHFL = 1024 };
+__host__ __device__ constexpr int DI(int k) { return ((SIDE * SIDE + 1) / 2 + k) / SIDE - SR; }
+__host__ __device__ constexpr int DJ(int k) { return ((SIDE * SIDE + 1) / 2 + k) % SIDE - SR; }
+__host__ __device__ constexpr int QB(int q) { return q >= 0 ? q / VW : -((-q + VW - 1) / VW); }
+__host__ __device__ constexpr int QR(int q) { return q - VW * QB(q); }
+union WV { int4 raw; float e[4]; };
+template <int F>
+__device__ __forceinline__ double cvt(float x) {
+  if (F & F_ICVT) {
+    const unsigned u = __float_as_uint(x);
+    return __hiloint2double((int)(__umulhi(u, 0x20000000u) + 0x38000000u), (int)(u << 29));
+  }
+  return (double)x;
+}
+__device__ __forceinline__ double fast_rsqrt(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));  // MUFU.RSQ64H: ~20 bits
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+template <int F, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_sweep(const float* __restrict__ w, const double* __restrict__ Din,
+                                                     double* Dout, int H, int W) {
+  extern __shared__ double vs[];
+  const int lane = threadIdx.x & 31, oi = threadIdx.x >> 5;
+  const int i0 = (blockIdx.y + 1) * TH, j0 = (blockIdx.x + 1) * TW;
+  const long long N = (long long)H * W;
+  if ((F & F_SMEM) && !(F & F_NOPRO)) {
+    for (int idx = threadIdx.x; idx < Y * X; idx += 256) {
+      const int ti = idx / X, tj = idx - ti * X;
+      const double* src = Din + (long long)(i0 - SR + ti) * W + (j0 - SR + tj);
+      if (F & F_ASYNC) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(vs + idx);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
+      } else {
+        vs[idx] = __ldg(src);
+      }
+    }
+    if (F & F_ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+  const int gi = i0 + oi, gj = j0 + VW * lane, ci = oi + SR, cj = VW * lane + SR;
+  const long long o = (long long)gi * W + gj;
+  double S[VW];
+#pragma unroll
+  for (int t = 0; t < VW; ++t) S[t] = (F & F_SMEM) ? vs[ci * X + cj + t] : 1.0;
+  float facc = 0.f;
+  if (F & F_ROWMAJOR) {
+#pragma unroll
+    for (int r = -SR; r <= SR; ++r) {
+      double v[VW + 2 * SR];
+      const double2* vrow = reinterpret_cast<const double2*>(vs + (ci + r) * X + VW * lane);
+#pragma unroll
+      for (int c = 0; c < (VW + 2 * SR) / 2; ++c) { const double2 t2 = vrow[c]; v[2 * c] = t2.x; v[2 * c + 1] = t2.y; }
+#pragma unroll
+      for (int dj = -SR; dj <= SR; ++dj) {
+        if (r == 0 && dj <= 0) continue;
+        if (r >= 0) {
+          const int k = (r + SR) * SIDE + dj + SR - (SIDE * SIDE + 1) / 2;
+          WV wp; wp.raw = __ldg(reinterpret_cast<const int4*>(w + (long long)k * N + o));
+#pragma unroll
+          for (int t = 0; t < VW; ++t) S[t] = fma(cvt<F>(wp.e[t]), v[t + dj + SR], S[t]);
+        }
+        if (r <= 0) {
+          const int di = -r, dj2 = (r == 0) ? dj : -dj;
+          const int k = (di + SR) * SIDE + dj2 + SR - (SIDE * SIDE + 1) / 2;
+          const long long om = (long long)k * N + o - (long long)di * W + VW * QB(-dj2);
+          WV lo, hi;
+          lo.raw = __ldg(reinterpret_cast<const int4*>(w + om));
+          if (QR(-dj2) != 0) {
+            if (F & F_SHFL) {
+#pragma unroll
+              for (int e = 0; e < QR(-dj2); ++e) hi.e[e] = __shfl_down_sync(0xffffffffu, lo.e[e], 1);
+              if (lane == 31) hi.raw = __ldg(reinterpret_cast<const int4*>(w + om + VW));
+            } else hi.raw = __ldg(reinterpret_cast<const int4*>(w + om + VW));
+          } else hi.raw = lo.raw;
+#pragma unroll
+          for (int t = 0; t < VW; ++t) {
+            const int u = t + QR(-dj2);
+            const double wm = cvt<F>(u < VW ? lo.e[u < VW ? u : 0] : hi.e[u >= VW ? u - VW : 0]);
+            S[t] = fma(wm, v[t - dj2 + SR], S[t]);
+          }
+        }
+      }
+    }
+  } else
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    constexpr int dummy = 0; (void)dummy;
+    const int di = DI(k), dj = DJ(k);
+    const float* wk = w + (long long)k * N;
+    WV wp, lo, hi;
+    wp.raw = __ldg(reinterpret_cast<const int4*>(wk + o));
+    if (F & F_MIRROR) {
+      const long long om = o - (long long)di * W + VW * QB(-dj);
+      lo.raw = __ldg(reinterpret_cast<const int4*>(wk + om));
+      if (QR(-dj) != 0) {
+        if (F & F_SHFL) {
+#pragma unroll
+          for (int e = 0; e < QR(-dj); ++e) hi.e[e] = __shfl_down_sync(0xffffffffu, lo.e[e], 1);
+          if (lane == 31) hi.raw = __ldg(reinterpret_cast<const int4*>(wk + om + VW));
+        } else hi.raw = __ldg(reinterpret_cast<const int4*>(wk + om + VW));
+      } else hi.raw = lo.raw;
+    }
+    if (F & F_FMA) {
+#pragma unroll
+      for (int t = 0; t < VW; ++t) {
+        const double vp = ((F & F_SMEM) && !(F & F_NOLDS)) ? vs[(ci + di) * X + cj + t + dj] : 1.25;
+        S[t] = fma(cvt<F>(wp.e[t]), vp, S[t]);
+        if (F & F_MIRROR) {
+          const int u = t + QR(-dj);
+          const double wm = cvt<F>(u < VW ? lo.e[u < VW ? u : 0] : hi.e[u >= VW ? u - VW : 0]);
+          const double vm = ((F & F_SMEM) && !(F & F_NOLDS)) ? vs[(ci - di) * X + cj + t - dj] : 0.75;
+          S[t] = fma(wm, vm, S[t]);
+        }
+      }
+    } else {
+      facc += wp.e[0] + wp.e[1] + wp.e[2] + wp.e[3];
+      if (F & F_MIRROR) facc += lo.e[0] + lo.e[3] + hi.e[0] + hi.e[3];
+    }
+  }
+  if (F & F_STORE) {
+#pragma unroll
+    for (int t = 0; t < VW; ++t) {
+      const double d = Din[o + t];
+      const double a = d * S[t] + (double)facc;
+      Dout[o + t] = (F & F_FASTEPI) ? d * fast_rsqrt(a) : d / sqrt(a);
+    }
+  } else if (S[0] + S[1] + S[2] + S[3] + (double)facc == 12345.678) Dout[0] = S[0];
+}
+template <class Fn>
+static float timeit(Fn f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  f(); f();
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) f();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return ms / 5;
+}
+static float* g_w; static double *g_d0, *g_d1; static int g_H, g_W;
+template <int F, int MINB>
+static void run(const char* name) {
+  dim3 grid(g_W / TW - 2, g_H / TH - 2);
+  const size_t sm = sizeof(double) * X * Y;
+  const float t = timeit([&] { k_sweep<F, MINB><<<grid, 256, sm>>>(g_w, g_d0, g_d1, g_H, g_W); });
+  const double gb = (double)NP * grid.x * grid.y * TW * TH * 4 / 1e9;
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, k_sweep<F, MINB>);
+  printf("%-34s minb %d regs %3d  %7.3f ms  %7.1f GB/s (planes)  %s\n", name, MINB, fa.numRegs, t, gb / t * 1e3,
+         cudaGetErrorString(cudaGetLastError()));
+}
+#define RUNALL(F, name) run<F, 5>(name); run<F, 4>(name); run<F, 3>(name); run<F, 2>(name);
+int main(int argc, char** argv) {
+  g_H = argc > 2 ? atoi(argv[1]) : 8192; g_W = argc > 2 ? atoi(argv[2]) : 8192;
+  const long long N = (long long)g_H * g_W;
+  cudaMalloc(&g_w, NP * N * 4); cudaMalloc(&g_d0, N * 8); cudaMalloc(&g_d1, N * 8);
+  cudaMemset(g_w, 0x3c, NP * N * 4);  // ~0.0115 per weight
+  cudaMemset(g_d0, 0x3f, N * 8);
+  constexpr int FULL = F_FMA | F_MIRROR | F_SMEM | F_STORE;
+  RUNALL(FULL, "full sweep")
+  RUNALL(FULL | F_ICVT, "full, int convert")
+  RUNALL(FULL | F_SHFL, "full, shuffled hi")
+  RUNALL(FULL | F_FASTEPI | F_ROWMAJOR, "full, fast epi, row-major")
+  RUNALL(FULL | F_FASTEPI | F_ROWMAJOR | F_ICVT, "full, fast epi, row-major, icvt")
+  RUNALL(FULL | F_FASTEPI | F_ROWMAJOR | F_ICVT | F_SHFL, "full, fast epi, row-major, icvt, shfl")
+  RUNALL(FULL | F_FASTEPI | F_ROWMAJOR | F_ICVT | F_SHFL | F_ASYNC, "all + async prologue")
+  RUNALL(FULL | F_FASTEPI | F_ICVT | F_SHFL | F_ASYNC, "all but row-major")
+  printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
