@@ -348,12 +348,43 @@ union WVec {
   WT e[16 / sizeof(WT)];
 };
 
+// Shared D tile of the vector sweep: the columns of a row are stored as VW
+// interleaved sub-rows (column c at (c % VW) * SUB + c / VW), so the 32 lanes
+// of a warp, whose columns are VW apart, read consecutive doubles (the plain
+// row layout is a 4-way bank conflict on every one of the 2 NP VW reads).
+// 1 / sqrt(a), a > 0 finite: MUFU.RSQ64H seed (~20 bits) + two Newton steps
+// (relative error ~1e-24 before the final rounding) -- 12 instructions where
+// sqrt + division take ~60; the balancing update then is d * rsqrt(d S),
+// within 2 ulp of d / sqrt(d S).
+__device__ __forceinline__ double pw_rsqrt(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+template <int SR, int VW>
+struct VTile {
+  static constexpr int X = 32 * VW + 2 * SR, SUB = (X + VW - 1) / VW, XS = VW * SUB;
+  __device__ static __forceinline__ int at(int row, int col) { return row * XS + (col % VW) * SUB + col / VW; }
+};
+
+// What each stage costs was measured on a stand-alone rebuild of this kernel
+// (tools/pw_sweep_probe.cu, DESIGN 3.4): the plane loads, converts and FMAs
+// alone run at the HBM roof; the tile prologue, the shared reads and the
+// epilogue each add time that does not overlap.  Hence: the tile arrives by
+// cp.async (one round trip instead of load -> store pairs), the first offset's
+// plane vectors are requested before the prologue's wait, the tile is bank-
+// conflict free, the epilogue takes d from the tile, 4 CTAs/SM (64 registers).
 template <int SR, typename WT>
-__global__ void __launch_bounds__(256, 5)  // 48 registers: 45.8 -> 43.1 ms per 8192^2 call
+__global__ void __launch_bounds__(256, 4)  // CTAs/SM of the vector sweep
     k_pw_sweep_v(PwArgs a, const double* Din, double* Dout,
                                                     int first, int apply) {
   constexpr int VW = 16 / sizeof(WT), TW = 32 * VW, TH = 8;
   constexpr int X = TW + 2 * SR, Y = TH + 2 * SR, NP = HalfPlane<SR>::NPOS;
+  using VT = VTile<SR, VW>;
   const int b = blockIdx.z;
   if (!takes_step(a.st[b], a.phase)) return;
   const int H = a.H, W = a.W;
@@ -362,72 +393,107 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 45.8 -> 43.1 ms per 
   const long long N = (long long)H * W;
   const double* Db = Din + (long long)b * N;
   const double* x = apply ? a.xin.at(b, a.st) : nullptr;
-  for (int idx = threadIdx.x; idx < Y * X; idx += blockDim.x) {
-    const int ti = idx / X, tj = idx - ti * X;
-    const long long o = (long long)wrap_fast(i0 - SR + ti, H) * W + wrap_fast(j0 - SR + tj, W);
-    const double d = first ? 1.0 : __ldg(Db + o);
-    vs[idx] = apply ? d * __ldg(x + o) : d;
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, oi = threadIdx.x >> 5;
   const int gj = j0 + VW * lane;
-  if (gj >= W) return;
   const int gi = min(i0 + oi, H - 1);  // rows past the image edge compute a throwaway copy
-  const int ci = gi - i0 + SR, cj = VW * lane + SR;
+  const int ci = gi - i0 + SR;
   const long long o = (long long)gi * W + gj;
   const WT* w0b = reinterpret_cast<const WT*>(a.w0) + (long long)b * NP * N;
+  const bool interior = i0 >= SR && i0 + TH + SR <= H && j0 >= 2 * VW && j0 + TW + 2 * VW <= W;
+  WVec<WT> wp0, lo0, hi0;  // offset 0 = (0, 1): requested before the tile is waited for
+  if (interior) {
+    constexpr int dj0 = HalfPlane<SR>::dj(0);
+    static_assert(HalfPlane<SR>::di(0) == 0 && VecSplit<VW>::qr(-dj0) != 0, "first offset is (0, 1)");
+    wp0.raw = __ldg(reinterpret_cast<const int4*>(w0b + o));
+    const long long om = o + VW * VecSplit<VW>::qb(-dj0);
+    lo0.raw = __ldg(reinterpret_cast<const int4*>(w0b + om));
+    hi0.raw = __ldg(reinterpret_cast<const int4*>(w0b + om + VW));
+  }
+  for (int idx = threadIdx.x; idx < Y * X; idx += blockDim.x) {
+    const int ti = idx / X, tj = idx - ti * X;
+    const long long q = (long long)wrap_fast(i0 - SR + ti, H) * W + wrap_fast(j0 - SR + tj, W);
+    double* dst = vs + VT::at(ti, tj);
+    if (first) {
+      *dst = apply ? __ldg(x + q) : 1.0;
+    } else if (apply) {
+      *dst = __ldg(Db + q) * __ldg(x + q);
+    } else {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                   "l"(Db + q));
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (gj >= W) return;
+  // v(row, m): tile row `row`, column VW * lane + m (m a compile-time constant)
+#define PW_V(row, m) vs[(row)*VT::XS + ((m) % VW) * VT::SUB + (m) / VW + lane]
   double S[VW];
 #pragma unroll
-  for (int t = 0; t < VW; ++t) S[t] = vs[ci * X + cj + t];
-  const bool interior = i0 >= SR && i0 + TH + SR <= H && j0 >= 2 * VW && j0 + TW + 2 * VW <= W;
+  for (int t = 0; t < VW; ++t) S[t] = PW_V(ci, SR + t);
   if (interior) {
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
       const WT* wk = w0b + (long long)k * N;
       WVec<WT> wp, lo, hi;
+      if (k == 0) {
+        wp = wp0;
+        lo = lo0;
+        hi = hi0;
+      } else {
+        wp.raw = __ldg(reinterpret_cast<const int4*>(wk + o));
+        const long long om = o - (long long)di * W + VW * VecSplit<VW>::qb(-dj);
+        lo.raw = __ldg(reinterpret_cast<const int4*>(wk + om));
+        if (VecSplit<VW>::qr(-dj) != 0) hi.raw = __ldg(reinterpret_cast<const int4*>(wk + om + VW));
+        else hi.raw = lo.raw;
+      }
+#pragma unroll
+      for (int t = 0; t < VW; ++t) {
+        const int u = t + VecSplit<VW>::qr(-dj);
+        const double wm = (double)(u < VW ? lo.e[u < VW ? u : 0] : hi.e[u >= VW ? u - VW : 0]);
+        S[t] = fma((double)wp.e[t], PW_V(ci + di, SR + t + dj), S[t]);
+        S[t] = fma(wm, PW_V(ci - di, SR + t - dj), S[t]);
+      }
+    }
+  } else {
+    // tiles on the periodic seam: the same vector loads with wrapped rows and
+    // vector columns (W % VW == 0: an aligned vector never straddles the seam)
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
+      const WT* wk = w0b + (long long)k * N;
+      const long long rm = (long long)wrap_fast(gi - di, H) * W;
+      const int cl = gj + VW * VecSplit<VW>::qb(-dj);
+      WVec<WT> wp, lo, hi;
       wp.raw = __ldg(reinterpret_cast<const int4*>(wk + o));
-      const long long om = o - (long long)di * W + VW * VecSplit<VW>::qb(-dj);
-      lo.raw = __ldg(reinterpret_cast<const int4*>(wk + om));
-      if (VecSplit<VW>::qr(-dj) != 0) hi.raw = __ldg(reinterpret_cast<const int4*>(wk + om + VW));
+      lo.raw = __ldg(reinterpret_cast<const int4*>(wk + rm + wrap_fast(cl, W)));
+      if (VecSplit<VW>::qr(-dj) != 0) hi.raw = __ldg(reinterpret_cast<const int4*>(wk + rm + wrap_fast(cl + VW, W)));
       else hi.raw = lo.raw;
 #pragma unroll
       for (int t = 0; t < VW; ++t) {
         const int u = t + VecSplit<VW>::qr(-dj);
         const double wm = (double)(u < VW ? lo.e[u < VW ? u : 0] : hi.e[u >= VW ? u - VW : 0]);
-        S[t] = fma((double)wp.e[t], vs[(ci + di) * X + cj + t + dj], S[t]);
-        S[t] = fma(wm, vs[(ci - di) * X + cj + t - dj], S[t]);
-      }
-    }
-  } else {
-#pragma unroll 1
-    for (int k = 0; k < NP; ++k) {
-      const int di = HalfPlane<SR>::di(k), dj = HalfPlane<SR>::dj(k);
-      const WT* wk = w0b + (long long)k * N;
-      const long long rm = (long long)wrap_fast(gi - di, H) * W;
-#pragma unroll
-      for (int t = 0; t < VW; ++t) {
-        const double wp = (double)__ldg(wk + o + t);
-        const double wm = (double)__ldg(wk + rm + wrap_fast(gj + t - dj, W));
-        S[t] = fma(wp, vs[(ci + di) * X + cj + t + dj], S[t]);
-        S[t] = fma(wm, vs[(ci - di) * X + cj + t - dj], S[t]);
+        S[t] = fma((double)wp.e[t], PW_V(ci + di, SR + t + dj), S[t]);
+        S[t] = fma(wm, PW_V(ci - di, SR + t - dj), S[t]);
       }
     }
   }
   if (i0 + oi >= H) return;
 #pragma unroll
   for (int t = 0; t < VW; ++t) {
-    const double d = first ? 1.0 : Db[o + t];
+    // the tile holds D itself on a balancing sweep (the same value as Db[o + t])
+    const double d = first ? 1.0 : (apply ? Db[o + t] : PW_V(ci, SR + t));
     if (apply) a.out[(long long)b * N + o + t] = d * S[t];
-    else Dout[(long long)b * N + o + t] = d / sqrt(d * S[t]);
+    else Dout[(long long)b * N + o + t] = d * pw_rsqrt(d * S[t]);
   }
+#undef PW_V
 }
 
 template <int SR, typename WT>
 static void pw_sweeps_v(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
   constexpr int VW = 16 / sizeof(WT), TW = 32 * VW;
   dim3 grid(cdivs(a.W, TW), cdivs(a.H, 8), a.B);
-  const size_t sm = sizeof(double) * (TW + 2 * SR) * (8 + 2 * SR);
+  const size_t sm = sizeof(double) * VTile<SR, VW>::XS * (8 + 2 * SR);
   const double* din = a.D0;
   double* dout = a.D1;
   for (int it = 0; it < a.iters; ++it) {
@@ -470,12 +536,13 @@ static void pw_pass_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_
   // with 4; 4096^2: 14.7 vs 21.8 ms) -- more, smaller CTAs hide the latency
   int rpt = 1;
   if (const char* e = getenv("REDVE_PW_RPT")) rpt = atoi(e);  // experiments
-  // the vector sweep pays on large images (4096^2 fp32: 13.8 -> 12.9 ms per
-  // call); below ~8 waves of its 4x larger CTAs the scalar sweep is faster
-  // (768^2 fp32: 0.69 vs 0.89 ms)
+  // the vector sweep (16-byte plane loads, cp.async tile, conflict-free tile
+  // layout, vector loads on the seam tiles too) is the faster one wherever it
+  // applies: per call 768^2 fp32 0.64 -> 0.47 ms, 512^2 0.42 -> 0.37, 2048^2
+  // 3.19 -> 2.74, fp64 planes 0.88 -> 0.76 at 768^2; level below 384^2 where
+  // the 22 launches dominate (tools/gpu_pw_sizes.sh)
   constexpr int VW = 16 / (int)sizeof(WT);
-  const long long vec_ctas = (long long)cdivs(a.W, 32 * VW) * cdivs(a.H, 8) * a.B;
-  bool vec = a.W % VW == 0 && a.W >= 32 * VW && vec_ctas >= 8LL * 148 * 4;
+  bool vec = a.W % VW == 0 && a.W >= 32 * VW;
   if (const char* e = getenv("REDVE_PW_VEC")) vec = e[0] == '1' ? (a.W % VW == 0 && a.W >= 32 * VW)
                                                                 : false;
   if (vec) {

@@ -7,9 +7,9 @@ run() {
   REDVE_PW_VEC=1 timeout 600 python bench.py --config 2 --no-cpu-baseline > $O/c2vec_$1.log 2>&1; python tools/show_bench.py $O/c2vec_$1.log | grep "value\|patch_w"
 }
 run a
-for mb in ${MINB:-4}; do
-  sed -i "s/__launch_bounds__(256, 5)  \/\/ 48 registers/__launch_bounds__(256, $mb)  \/\/ 48 registers/" paper_1805_02158_b200/csrc/sr.cu
+for mb in ${MINB:-5}; do
+  sed -i "s/__launch_bounds__(256, 4)  \/\/ CTAs\/SM of the vector sweep/__launch_bounds__(256, $mb)  \/\/ CTAs\/SM of the vector sweep/" paper_1805_02158_b200/csrc/sr.cu
   (cd paper_1805_02158_b200/csrc && make -j8 > /dev/null 2>&1; grep -A2 "k_pw_sweep_vILi3EfEE" build/sr.ptxas.log | tail -2)
   run mb$mb
-  sed -i "s/__launch_bounds__(256, $mb)  \/\/ 48 registers/__launch_bounds__(256, 5)  \/\/ 48 registers/" paper_1805_02158_b200/csrc/sr.cu
+  sed -i "s/__launch_bounds__(256, $mb)  \/\/ CTAs\/SM of the vector sweep/__launch_bounds__(256, 4)  \/\/ CTAs\/SM of the vector sweep/" paper_1805_02158_b200/csrc/sr.cu
 done
