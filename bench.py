@@ -583,6 +583,16 @@ def ncu_traffic(kind):
     return None if v is None else float(v)
 
 
+def ncu_traffic_for(kind, config):
+    """Per-launch DRAM traffic of `kind` on `config`: config-keyed entries
+    ("patch_weighted:c4": the composite's kernels summed over one call) first,
+    the configs[1] kernel table otherwise."""
+    v = ncu_traffic(f"{kind}:c{config}")
+    if v is None and config == 1:
+        v = ncu_traffic(kind)
+    return v
+
+
 def init_ranks(world, local):
     """One rank per GPU over NCCL.  When the node has fewer GPUs than ranks
     (plumbing checks on a 1-GPU box), ranks share devices round-robin and the
@@ -773,7 +783,7 @@ def run_native(a):
                 "frac": None if ach is None else ach / peak, "peak_source": peak_src,
                 "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
                 "algorithmic_bytes_per_launch": algorithmic_bytes(dom, B, N, ws=_pw_ws(c)),
-                "traffic": ncu_traffic(dom) if a.config == 1 else None}
+                "traffic": ncu_traffic_for(dom, a.config)}
 
     # whole-step roofline against SURVEY.md 8(d)'s per-iteration algorithmic
     # bytes for the deblur step, N s (2 + 7.5 + 2 + 1 + (2k+3)/(m+k+1) + 4/c)
@@ -994,7 +1004,7 @@ def run_spatial(a):
             "share_of_step": kernels[dom]["total_ms"] / step_kernel_ms,
             "algorithmic_bytes_per_launch": algorithmic_bytes(
                 dom, 1, ext_rows[dom] * n if dom in ext_rows else lay.rows * n, ws=_pw_ws(c)),
-                "traffic": None}
+            "traffic": ncu_traffic_for(dom, 4)}
 
     # e2e through the public API: problem setup from the host measurements (H2D of
     # the slab's y and x0), the solve, the gathered host image out.  The timed
