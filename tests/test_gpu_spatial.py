@@ -86,20 +86,27 @@ def test_window_gram_decide_combine(pair, method):
     assert rel(out.ravel(), ref["vector"]) <= 1e-10
 
 
-def _native_spatial(H, W, method, budget, ve_method, den_name="median", comm=None):
+def _native_spatial(H, W, method, budget, ve_method, den_name="median", comm=None, pinned=False):
     from paper_1805_02158_b200 import Median3, PatchWeighted
     from paper_1805_02158_b200.solvers import SolveConfig
-    from paper_1805_02158_b200.spatial import PeerComm, SpatialProblem, TorchComm, solve_spatial
+    from paper_1805_02158_b200.spatial import (PeerComm, PinnedHost, SpatialProblem, TorchComm,
+                                               solve_spatial)
 
     if comm == "peer":                     # built inside the rank process
         comm = PeerComm(device="cpu")
 
     taps, op, truth, y, _, _, x0 = _setup(H, W, "median")
     den = Median3() if den_name == "median" else PatchWeighted(1, 1, 110.0, 3)
+    out = None
+    if pinned:  # page-locked host images in, result into a caller-owned pinned buffer
+        y, x0, truth, out = PinnedHost(y), PinnedHost(x0), PinnedHost(truth), PinnedHost(shape=(H, W))
     prob = SpatialProblem(_Fwd(taps, FACTOR, (H, W)), y, SIGMA, ALPHA, den,
                           comm=comm or TorchComm(), reference=truth)
     cfg = SolveConfig(method=method, ve_method=ve_method, max_inner_steps=budget)
-    x, tr = solve_spatial(prob, x0, cfg)
+    x, tr = solve_spatial(prob, x0, cfg, out=out)
+    if pinned:
+        assert np.shares_memory(x, out.numpy()) and out.t.is_pinned()
+        x = x.copy()
     return (x, np.array([r.step_norm for r in tr.records]),
             np.array([np.nan if r.cost is None else r.cost for r in tr.records]),
             np.array([np.nan if r.psnr is None else r.psnr for r in tr.records]))
@@ -169,6 +176,14 @@ def test_two_ranks_native_solve():
     for k in range(4):
         np.testing.assert_array_equal(out[0][k], out[1][k])
     _check(out[0], H, W, "fp-ve", budget, "rre")
+
+
+def test_pinned_host_images_equal_numpy_images():
+    """PinnedHost inputs / output buffer: the same solve, bit for bit."""
+    got = _native_spatial(96, 90, "fp-ve", 14, "rre", pinned=True)
+    ref = _native_spatial(96, 90, "fp-ve", 14, "rre")
+    for k in range(4):
+        np.testing.assert_array_equal(got[k], ref[k])
 
 
 # ---- peer-memory halo exchange (PeerComm / redve_halo_push) ----------------

@@ -33,7 +33,7 @@ for rep in range(2):
     xs = prob.slab(x0)
     t2 = tick()
     g = prob.gather
-    prob.gather = lambda x: x
+    prob.gather = lambda x, out=None: x
     xd, tr = solve_spatial(prob, xs, cfg)
     t3 = tick()
     xh = g(xd)
