@@ -444,7 +444,8 @@ class TestPatchWeightedFp32Planes:
         assert e2 <= 1e-6
 
     @pytest.mark.parametrize("wdt", ["float32", "float64"])
-    @pytest.mark.parametrize("shape", [(136, 260), (24, 520), (256, 256), (40, 128)])
+    @pytest.mark.parametrize("shape", [(136, 260), (24, 520), (256, 256), (40, 128), (43, 132),
+                                       (61, 388)])  # the last two: rows past the last full tile
     def test_vector_sweep_vs_oracle(self, rv, R, monkeypatch, wdt, shape):
         # the vectorised sweep (picked automatically only for large images)
         monkeypatch.setenv("REDVE_PW_VEC", "1")
