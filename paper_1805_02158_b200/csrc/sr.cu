@@ -378,11 +378,11 @@ struct VTile {
 // cp.async (one round trip instead of load -> store pairs), the first offset's
 // plane vectors are requested before the prologue's wait, the tile is bank-
 // conflict free, the epilogue takes d from the tile, 4 CTAs/SM (64 registers).
-template <int SR, typename WT>
-__global__ void __launch_bounds__(256, 4)  // CTAs/SM of the vector sweep
+template <int SR, typename WT, int TH = 8>  // TH tile rows = warps per CTA
+__global__ void __launch_bounds__(32 * TH, 32 / TH)  // 1024 threads/SM (64 registers)
     k_pw_sweep_v(PwArgs a, const double* Din, double* Dout,
                                                     int first, int apply) {
-  constexpr int VW = 16 / sizeof(WT), TW = 32 * VW, TH = 8;
+  constexpr int VW = 16 / sizeof(WT), TW = 32 * VW;
   constexpr int X = TW + 2 * SR, Y = TH + 2 * SR, NP = HalfPlane<SR>::NPOS;
   using VT = VTile<SR, VW>;
   const int b = blockIdx.z;
@@ -489,21 +489,21 @@ __global__ void __launch_bounds__(256, 4)  // CTAs/SM of the vector sweep
 #undef PW_V
 }
 
-template <int SR, typename WT>
+template <int SR, typename WT, int TH>
 static void pw_sweeps_v(const PwArgs& a, cudaStream_t s, int* launches, bool with_apply) {
   constexpr int VW = 16 / sizeof(WT), TW = 32 * VW;
-  dim3 grid(cdivs(a.W, TW), cdivs(a.H, 8), a.B);
-  const size_t sm = sizeof(double) * VTile<SR, VW>::XS * (8 + 2 * SR);
+  dim3 grid(cdivs(a.W, TW), cdivs(a.H, TH), a.B);
+  const size_t sm = sizeof(double) * VTile<SR, VW>::XS * (TH + 2 * SR);
   const double* din = a.D0;
   double* dout = a.D1;
   for (int it = 0; it < a.iters; ++it) {
-    k_pw_sweep_v<SR, WT><<<grid, 256, sm, s>>>(a, din, dout, it == 0, 0);
+    k_pw_sweep_v<SR, WT, TH><<<grid, 32 * TH, sm, s>>>(a, din, dout, it == 0, 0);
     ++*launches;
     din = dout;
     dout = (dout == a.D1) ? a.D0 : a.D1;
   }
   if (with_apply) {
-    k_pw_sweep_v<SR, WT><<<grid, 256, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
+    k_pw_sweep_v<SR, WT, TH><<<grid, 32 * TH, sm, s>>>(a, din, nullptr, a.iters == 0, 1);
     ++*launches;
   }
 }
@@ -546,7 +546,13 @@ static void pw_pass_t(const PwArgs& a, cudaStream_t s, int* launches, bool with_
   if (const char* e = getenv("REDVE_PW_VEC")) vec = e[0] == '1' ? (a.W % VW == 0 && a.W >= 32 * VW)
                                                                 : false;
   if (vec) {
-    pw_sweeps_v<SR, WT>(a, s, launches, with_apply);
+    // 16-row tiles (512 threads): 1.375x instead of 1.75x of the D tile is halo and
+    // fewer mirrored rows fall outside the CTA: 365 -> 360 us per 768^2 call,
+    // 38.1 -> 37.6 ms per 8192^2 call
+    int th = a.H >= 64 ? 16 : 8;
+    if (const char* e = getenv("REDVE_PW_TH")) th = atoi(e);  // experiments
+    if (th == 16) pw_sweeps_v<SR, WT, 16>(a, s, launches, with_apply);
+    else pw_sweeps_v<SR, WT, 8>(a, s, launches, with_apply);
     return;
   }
   if (rpt == 4) pw_sweeps_t<SR, 4, WT>(a, s, launches, with_apply);
